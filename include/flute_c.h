@@ -1,0 +1,139 @@
+/* flute-b200 — C ABI of the B200 LUT-GEMM hot path.
+ *
+ * Plain C, plain pointers and sizes, no torch / CUDA types in the signatures
+ * (streams are passed as void* = cudaStream_t).  Every entry point names the
+ * reference interface it replaces (reference tree: /root/reference/proj).
+ *
+ * Status codes mirror the reference's exception taxonomy (errors.hpp:12-50):
+ *   FLUTE_OK, FLUTE_ERR_CONFIG (ConfigError), FLUTE_ERR_INPUT (InputError),
+ *   FLUTE_ERR_INTERNAL (InternalError), FLUTE_ERR_CUDA (CUDA runtime/driver).
+ * flute_last_error() returns the message of the last failure on the calling
+ * thread.  Nothing here falls back to the CPU: device entry points fail with
+ * FLUTE_ERR_CUDA when no sm_100 device is usable.
+ *
+ * Index/scale/table conventions (quantize.hpp:17-39, vec_lut.hpp:18-30):
+ *   indices  u8  [k][n] row-major, each < 2^bits
+ *   scales   f16 [n][k/group] (column-major over groups), as raw u16 bits
+ *   table    2^bits f32 values (narrowed to f16 exactly as the reference does)
+ *   vLUT     2^(2*bits) u32 words: low half = T[i] (even k), high = T[j]
+ *   x        f16 [m][k] row-major; y f16 [m][n] row-major
+ */
+#ifndef FLUTE_C_H
+#define FLUTE_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLUTE_OK 0
+#define FLUTE_ERR_CONFIG 1
+#define FLUTE_ERR_INPUT 2
+#define FLUTE_ERR_INTERNAL 3
+#define FLUTE_ERR_CUDA 4
+
+const char* flute_last_error(void);
+const char* flute_version(void);
+
+/* ---- numerics (half.hpp:81-93) ------------------------------------------ */
+uint16_t flute_f32_to_f16(float x);
+float flute_f16_to_f32(uint16_t h);
+
+/* ---- input producers (nf_table.hpp:48, quantize.hpp:45-52) --------------- */
+int flute_nf_table(int bits, float* values_out /* 2^bits */);
+int flute_quantize(const float* w /* k x n */, int k, int n, int bits, int group,
+                   uint8_t* indices_out, uint16_t* scales_out);
+
+/* ---- canonical packer: reorder_and_split / unpack_matrix (pack.hpp:72-85) */
+/* layout = {tile_m, tile_n, tile_k, frag_m, frag_n, frag_k} (pack.hpp:20-37).
+ * slice_hi holds ceil(k*n*w/32) words (w = 2 for 3-bit, else bits); slice_lo
+ * (3-bit only, may be NULL otherwise) holds ceil(k*n/32) words. */
+size_t flute_canonical_words(int k, int n, int slice_bits);
+int flute_pack_canonical(const uint8_t* indices, int k, int n, int bits, const int* layout,
+                         uint32_t* slice_hi, uint32_t* slice_lo);
+int flute_unpack_canonical(const uint32_t* slice_hi, const uint32_t* slice_lo, int k, int n,
+                           int bits, const int* layout, uint8_t* indices_out);
+
+/* ---- sm_100a device layout (new) --------------------------- */
+int flute_device_sizes(int k, int n, int bits, int group, size_t* weight_bytes,
+                       size_t* scale_bytes);
+int flute_pack_device(const uint8_t* indices, int k, int n, int bits, int group,
+                      uint8_t* out /* weight_bytes */);
+int flute_repack_canonical(const uint32_t* slice_hi, const uint32_t* slice_lo, int k, int n,
+                           int bits, const int* layout, int group, uint8_t* out);
+int flute_unpack_device(const uint8_t* packed, int k, int n, int bits, int group,
+                        uint8_t* indices_out);
+int flute_scales_device(const uint16_t* scales, int k, int n, int group,
+                        uint16_t* out /* scale_bytes/2 */);
+
+/* ---- vectorized LUT: make_vectorized_lut / vec_dequantize (vec_lut.hpp:34-43) */
+/* out: 2^(2b)*dup words, copy c of entry e at e*dup + c. */
+int flute_vlut_build(const float* table_values, int bits, int dup, uint32_t* out);
+/* dup-1 vLUT -> the 2^(2b) words in device-index order (identity for 2/4-bit). */
+int flute_vlut_device_words(const uint32_t* vlut_words, int bits, uint32_t* out);
+int flute_vec_dequantize(uint32_t pair, uint16_t scale, const uint32_t* vlut_words, int bits,
+                         uint32_t* out /* first | second << 16 */);
+
+/* ---- Stream-K plan (streamk.hpp:58) + traffic model (engine.hpp:74-96) --- */
+/* ranges: 2*workers; fixups (nullable): 4 per split tile {tile, finisher,
+ * slot_base, n_contributors}. */
+int flute_plan_stream_k(int tiles_m, int tiles_n, int tiles_k, int workers, int64_t* ranges,
+                        int64_t* fixups, int max_fixups, int* n_fixups, int64_t* total_slots);
+/* stats: {weights, scales, table, activations, partials_rw, output, flops}. */
+int flute_plan_traffic(int m, int k, int n, int bits, int group, const int* layout, int workers,
+                       int stages, int tile_m, uint64_t* stats);
+double flute_bits_per_param(int bits, int group);
+
+/* ---- device: the qgemm (engine.hpp:72 execute, "qgemm" of the paper) ----- */
+int flute_device_count(void);
+int flute_sm_count(int device);
+/* Largest Stream-K CTA count that is guaranteed co-resident for an m-row call
+ * (the finisher/contributor handshake needs every CTA resident). */
+int flute_max_workers(int m);
+/* Default worker count (CTAs) for a shape. */
+int flute_default_workers(int m, int k, int n, int bits);
+
+/* Raw device-pointer GEMM.  w / scales in device layout, vlut = the 2^(2b)
+ * device-order words, all in device memory.  workspace: >=
+ * flute_workspace_bytes(m, workers) bytes of device memory, zero-filled
+ * before first use (the kernel leaves it zeroed).  One workspace must not be
+ * used by two launches that may run concurrently.  workers <= 0 picks the
+ * default.  Async on `stream` (cudaStream_t; NULL = legacy default). */
+size_t flute_workspace_bytes(int m, int workers);
+int flute_qgemm(const void* x, int m, int k, int n, const void* w, const void* scales,
+                const void* vlut, int bits, int group, void* y, void* workspace,
+                size_t workspace_bytes, int workers, void* stream);
+
+/* Device-resident weight handle: uploads device-layout weights, scales and the
+ * vLUT once (flute_weights_create*), owns a workspace. */
+typedef struct flute_weights flute_weights;
+int flute_weights_create(const uint8_t* packed_host, const uint16_t* scales_dev_layout_host,
+                         const uint32_t* vlut_words /* dup 1, reference order */, int k, int n,
+                         int bits, int group, flute_weights** out);
+/* Convenience: from indices [k][n] + scales [n][k/g] + table values. */
+int flute_weights_from_indices(const uint8_t* indices, const uint16_t* scales,
+                               const float* table_values, int k, int n, int bits, int group,
+                               flute_weights** out);
+int flute_weights_destroy(flute_weights* w);
+int flute_weights_info(const flute_weights* w, int* k, int* n, int* bits, int* group);
+int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int workers,
+               void* stream);
+/* End-to-end: x and y are HOST pointers; copies in, GEMM, copies out, syncs. */
+int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
+                    int workers, void* stream);
+
+/* ---- device self-checks (used by the parity tests) ----------------------- */
+/* Run the kernel's own dequant routine over every pair x every scale:
+ * out[s * 2^(2b) + p] = device half2 for (pair p, scales[s]); pair p in
+ * reference order (the routine applies the device index permutation). */
+int flute_dequant_all_device(const uint32_t* vlut_words, int bits, const uint16_t* scales,
+                             int n_scales, uint32_t* out_host);
+/* mma_fragment on the tensor cores (mma.hpp:23); host buffers. */
+int flute_mma_fragment(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLUTE_C_H */

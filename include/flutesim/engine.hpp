@@ -1,0 +1,116 @@
+// flute-b200 — the fused LUT-dequant matmul ("qgemm").
+//
+// Drop-in for the reference engine (reference: proj/include/flutesim/
+// engine.hpp:24-96, engine.cpp:345-418).  execute() keeps the reference's
+// signature, validation and exception classes, but the work runs on the B200:
+// the packed weights are re-laid into sm_100a fragment order, uploaded, and one
+// Stream-K kernel does TMA-fed dequant + tensor-core MMA with a deterministic
+// fp32 cross-CTA fixup.  Results are bitwise identical across runs, ExecMode
+// and `stages`; `workers` is the Stream-K CTA count.
+//
+// TrafficStats keeps the reference's *accounting model* (engine.cpp:87-130):
+// execute().stats == plan_traffic(shape) exactly, as the reference guarantees.
+// It is not a measurement of the GPU kernel (use ncu / bench.py for that).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+
+#include "flutesim/matrix.hpp"
+#include "flutesim/pack.hpp"
+#include "flutesim/quantize.hpp"
+#include "flutesim/streamk.hpp"
+#include "flutesim/vec_lut.hpp"
+
+namespace flutesim {
+
+struct TrafficStats {
+  std::uint64_t bytes_weights = 0;
+  std::uint64_t bytes_scales = 0;
+  std::uint64_t bytes_table = 0;
+  std::uint64_t bytes_activations = 0;
+  std::uint64_t bytes_partials_rw = 0;
+  std::uint64_t bytes_output = 0;
+  std::uint64_t flops = 0;
+
+  std::uint64_t total_bytes() const {
+    return bytes_weights + bytes_scales + bytes_table + bytes_activations + bytes_partials_rw +
+           bytes_output;
+  }
+  double arithmetic_intensity() const {
+    return total_bytes() == 0 ? 0.0
+                              : static_cast<double>(flops) / static_cast<double>(total_bytes());
+  }
+  TrafficStats& operator+=(const TrafficStats& o);
+};
+
+enum class ExecMode {
+  kSerial,    // accepted for API compatibility; same GPU kernel, same bits
+  kParallel,
+};
+
+struct MatmulProblem {
+  const MatH* x = nullptr;
+  const PackedWeights* weights = nullptr;
+  const std::vector<Half>* scales = nullptr;
+  const VectorizedTable* lut = nullptr;
+  QuantConfig cfg;
+  int workers = 1;   // Stream-K CTAs on the device
+  int stages = 2;    // validated (>= 1); the device pipeline depth is its own
+  int tile_m = 0;
+  ExecMode mode = ExecMode::kParallel;
+};
+
+struct MatmulResult {
+  MatH y;
+  TrafficStats stats;
+};
+
+MatmulResult execute(const MatmulProblem& problem);
+
+double bits_per_param(const QuantConfig& cfg);
+double weight_traffic_ratio(const TrafficStats& stats, double dense_weight_bytes);
+
+struct ProblemShape {
+  int m = 1;
+  int k = 0;
+  int n = 0;
+  QuantConfig cfg;
+  LayoutDescriptor layout;
+  int workers = 1;
+  int stages = 2;
+  int dup = 1;
+  int tile_m = 0;
+};
+TrafficStats plan_traffic(const ProblemShape& shape);
+
+// ---------------------------------------------------------------------------
+// Device-resident path (new): upload once, call many times.
+// ---------------------------------------------------------------------------
+
+class DeviceWeights {
+ public:
+  // From the canonical packed form + scales + vLUT (what execute() receives).
+  DeviceWeights(const PackedWeights& pw, const std::vector<Half>& scales,
+                const VectorizedTable& lut, const QuantConfig& cfg);
+  // From a raw index matrix [k][n] + [n][k/g] scales + table values.
+  DeviceWeights(const std::vector<std::uint8_t>& indices, const std::vector<Half>& scales,
+                const LookupTable& table, int k, int n, const QuantConfig& cfg);
+  ~DeviceWeights();
+  DeviceWeights(const DeviceWeights&) = delete;
+  DeviceWeights& operator=(const DeviceWeights&) = delete;
+
+  int k() const;
+  int n() const;
+  // y_dev[m][n] = x_dev[m][k] * W_hat, device pointers, async on `stream`.
+  void gemm(const Half* x_dev, int m, Half* y_dev, int workers = 0, void* stream = nullptr);
+  // Host in / host out (copies inside; synchronizes the stream).
+  MatH gemm_host(const MatH& x, int workers = 0, void* stream = nullptr);
+
+  struct Impl;
+
+ private:
+  std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace flutesim

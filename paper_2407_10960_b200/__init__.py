@@ -1,0 +1,442 @@
+"""flute-b200 — B200-native LUT-quantized GEMM (FLUTE, arXiv 2407.10960).
+
+Python front-end over the C ABI in ``include/flute_c.h`` (the product is the
+C++/CUDA library ``libflute_b200.so`` next to this file).  Names follow the
+reference C++ API (``reorder_and_split``, ``make_vectorized_lut``,
+``plan_stream_k``, ``execute`` …; reference: /root/reference/proj/include/
+flutesim/*.hpp) so that tests read like the reference's own.
+
+There is no CPU fallback: GPU entry points raise :class:`CudaError` when the
+library or an sm_100 device is unavailable, and importing this package fails
+loudly if the shared library has not been built (``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflute_b200.so")
+
+DEFAULT_LAYOUT = (16, 64, 64, 16, 8, 16)  # reference pack.hpp:21-26
+UNIT_N, UNIT_K = 64, 128                  # device Stream-K unit (pack.hpp kUnitN/kUnitK)
+
+
+class FluteError(RuntimeError):
+    code = 0
+
+
+class ConfigError(FluteError):
+    code = 1
+
+
+class InputError(FluteError):
+    code = 2
+
+
+class InternalError(FluteError):
+    code = 3
+
+
+class CudaError(FluteError):
+    code = 4
+
+
+_ERRS = {1: ConfigError, 2: InputError, 3: InternalError, 4: CudaError}
+
+
+def build(force: bool = False) -> str:
+    """Compile the product library in-tree (nvcc for sm_100a + g++)."""
+    if force:
+        subprocess.run(["make", "-s", "-C", os.path.join(_HERE, "csrc"), "clean"], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", os.path.join(_HERE, "csrc")], check=True)
+    return LIB_PATH
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    return C.CDLL(LIB_PATH)
+
+
+_lib = _load()
+
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+
+# Every symbol include/flute_c.h declares, with its ctypes signature.
+_SIGS = {
+    "flute_last_error": (C.c_char_p, []),
+    "flute_version": (C.c_char_p, []),
+    "flute_f32_to_f16": (C.c_uint16, [C.c_float]),
+    "flute_f16_to_f32": (C.c_float, [C.c_uint16]),
+    "flute_nf_table": (C.c_int, [C.c_int, _f32p]),
+    "flute_quantize": (C.c_int, [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _u16p]),
+    "flute_canonical_words": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "flute_pack_canonical": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, _i32p, _u32p, _vp]),
+    "flute_unpack_canonical": (C.c_int, [_u32p, _vp, C.c_int, C.c_int, C.c_int, _i32p, _u8p]),
+    "flute_device_sizes": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "flute_pack_device": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p]),
+    "flute_repack_canonical": (C.c_int, [_u32p, _vp, C.c_int, C.c_int, C.c_int, _i32p, C.c_int,
+                                         _u8p]),
+    "flute_unpack_device": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p]),
+    "flute_scales_device": (C.c_int, [_u16p, C.c_int, C.c_int, C.c_int, _u16p]),
+    "flute_vlut_build": (C.c_int, [_f32p, C.c_int, C.c_int, _u32p]),
+    "flute_vlut_device_words": (C.c_int, [_u32p, C.c_int, _u32p]),
+    "flute_vec_dequantize": (C.c_int, [C.c_uint32, C.c_uint16, _u32p, C.c_int,
+                                       C.POINTER(C.c_uint32)]),
+    "flute_plan_stream_k": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _i64p, _vp, C.c_int,
+                                      C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
+    "flute_plan_traffic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32p, C.c_int,
+                                     C.c_int, C.c_int, _u64p]),
+    "flute_bits_per_param": (C.c_double, [C.c_int, C.c_int]),
+    "flute_device_count": (C.c_int, []),
+    "flute_sm_count": (C.c_int, [C.c_int]),
+    "flute_max_workers": (C.c_int, [C.c_int]),
+    "flute_default_workers": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "flute_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "flute_qgemm": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, C.c_int,
+                              _vp, _vp, C.c_size_t, C.c_int, _vp]),
+    "flute_weights_create": (C.c_int, [_u8p, _u16p, _u32p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(_vp)]),
+    "flute_weights_from_indices": (C.c_int, [_u8p, _u16p, _f32p, C.c_int, C.c_int, C.c_int,
+                                             C.c_int, C.POINTER(_vp)]),
+    "flute_weights_destroy": (C.c_int, [_vp]),
+    "flute_weights_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "flute_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _vp]),
+    "flute_gemm_host": (C.c_int, [_vp, _u16p, C.c_int, _u16p, C.c_int, _vp]),
+    "flute_dequant_all_device": (C.c_int, [_u32p, C.c_int, _u16p, C.c_int, _u32p]),
+    "flute_mma_fragment": (C.c_int, [_u16p, _u16p, _f32p, C.c_int, C.c_int, C.c_int]),
+}
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)  # AttributeError here = a declared symbol is not exported
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _ERRS.get(rc, FluteError)(_lib.flute_last_error().decode())
+
+
+def _lay(layout) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(layout, np.int32))
+
+
+def version() -> str:
+    return _lib.flute_version().decode()
+
+
+# --------------------------------------------------------------------------
+# numerics + input producers
+# --------------------------------------------------------------------------
+
+def f32_to_f16(x: float) -> int:
+    return int(_lib.flute_f32_to_f16(float(x)))
+
+
+def f16_to_f32(h: int) -> float:
+    return float(_lib.flute_f16_to_f32(int(h)))
+
+
+def build_nf_table(bits: int) -> np.ndarray:
+    out = np.zeros(1 << bits, np.float32)
+    _check(_lib.flute_nf_table(bits, out))
+    return out
+
+
+def quantize_matrix(w: np.ndarray, bits: int, group: int):
+    """quantize.hpp:45 — returns (indices u8 [k][n], scales u16 [n][k/g])."""
+    w = np.ascontiguousarray(w, np.float32)
+    k, n = w.shape
+    idx = np.zeros((k, n), np.uint8)
+    sc = np.zeros(k * n // max(group, 1), np.uint16)
+    _check(_lib.flute_quantize(w, k, n, bits, group, idx, sc))
+    return idx, sc
+
+
+# --------------------------------------------------------------------------
+# packers
+# --------------------------------------------------------------------------
+
+def canonical_words(k: int, n: int, slice_bits: int) -> int:
+    return int(_lib.flute_canonical_words(k, n, slice_bits))
+
+
+def reorder_and_split(indices: np.ndarray, bits: int, layout=DEFAULT_LAYOUT):
+    """pack.hpp:72 — canonical slices (hi[, lo]) as u32 arrays."""
+    idx = np.ascontiguousarray(indices, np.uint8)
+    k, n = idx.shape
+    hi = np.zeros(max(1, canonical_words(k, n, 2 if bits == 3 else bits)), np.uint32)
+    lo = np.zeros(max(1, canonical_words(k, n, 1)), np.uint32) if bits == 3 else None
+    _check(_lib.flute_pack_canonical(idx, k, n, bits, _lay(layout), hi,
+                                     lo.ctypes.data if lo is not None else None))
+    return (hi, lo) if bits == 3 else (hi,)
+
+
+def unpack_matrix(slices, k: int, n: int, bits: int, layout=DEFAULT_LAYOUT) -> np.ndarray:
+    hi = np.ascontiguousarray(slices[0], np.uint32)
+    lo = np.ascontiguousarray(slices[1], np.uint32) if bits == 3 else None
+    out = np.zeros((k, n), np.uint8)
+    _check(_lib.flute_unpack_canonical(hi, lo.ctypes.data if lo is not None else None, k, n, bits,
+                                       _lay(layout), out))
+    return out
+
+
+def device_sizes(k: int, n: int, bits: int, group: int):
+    wb, sb = C.c_size_t(0), C.c_size_t(0)
+    _check(_lib.flute_device_sizes(k, n, bits, group, C.byref(wb), C.byref(sb)))
+    return wb.value, sb.value
+
+
+def pack_device(indices: np.ndarray, bits: int, group: int) -> np.ndarray:
+    idx = np.ascontiguousarray(indices, np.uint8)
+    k, n = idx.shape
+    wb, _ = device_sizes(k, n, bits, group)
+    out = np.zeros(wb, np.uint8)
+    _check(_lib.flute_pack_device(idx, k, n, bits, group, out))
+    return out
+
+
+def repack_canonical(slices, k: int, n: int, bits: int, group: int, layout=DEFAULT_LAYOUT):
+    hi = np.ascontiguousarray(slices[0], np.uint32)
+    lo = np.ascontiguousarray(slices[1], np.uint32) if bits == 3 else None
+    wb, _ = device_sizes(k, n, bits, group)
+    out = np.zeros(wb, np.uint8)
+    _check(_lib.flute_repack_canonical(hi, lo.ctypes.data if lo is not None else None, k, n, bits,
+                                       _lay(layout), group, out))
+    return out
+
+
+def unpack_device(packed: np.ndarray, k: int, n: int, bits: int, group: int) -> np.ndarray:
+    out = np.zeros((k, n), np.uint8)
+    _check(_lib.flute_unpack_device(np.ascontiguousarray(packed, np.uint8), k, n, bits, group,
+                                    out))
+    return out
+
+
+def scales_device(scales: np.ndarray, k: int, n: int, group: int) -> np.ndarray:
+    _, sb = device_sizes(k, n, 4, group)
+    out = np.zeros(sb // 2, np.uint16)
+    _check(_lib.flute_scales_device(np.ascontiguousarray(scales, np.uint16), k, n, group, out))
+    return out
+
+
+# --------------------------------------------------------------------------
+# vLUT
+# --------------------------------------------------------------------------
+
+def make_vectorized_lut(table_values: np.ndarray, bits: int, dup: int = 1) -> np.ndarray:
+    """vec_lut.hpp:34 — 2^(2b)*dup u32 words (first | second << 16)."""
+    out = np.zeros((1 << (2 * bits)) * max(dup, 1), np.uint32)
+    _check(_lib.flute_vlut_build(np.ascontiguousarray(table_values, np.float32), bits, dup, out))
+    return out
+
+
+def vlut_device_words(vlut_words: np.ndarray, bits: int) -> np.ndarray:
+    out = np.zeros(1 << (2 * bits), np.uint32)
+    _check(_lib.flute_vlut_device_words(np.ascontiguousarray(vlut_words, np.uint32), bits, out))
+    return out
+
+
+def vec_dequantize(pair: int, scale: int, vlut_words: np.ndarray, bits: int) -> int:
+    o = C.c_uint32(0)
+    _check(_lib.flute_vec_dequantize(pair, scale, np.ascontiguousarray(vlut_words, np.uint32),
+                                     bits, C.byref(o)))
+    return o.value
+
+
+# --------------------------------------------------------------------------
+# Stream-K + traffic
+# --------------------------------------------------------------------------
+
+@dataclass
+class StreamKPlan:
+    ranges: np.ndarray   # [workers, 2]
+    fixups: np.ndarray   # [n_fixups, 4] (tile, finisher, slot_base, n_contributors)
+    total_slots: int
+
+
+def plan_stream_k(tiles_m: int, tiles_n: int, tiles_k: int, workers: int) -> StreamKPlan:
+    ranges = np.zeros(2 * max(workers, 1), np.int64)
+    cap = max(tiles_m * tiles_n, 1)
+    fx = np.zeros(4 * cap, np.int64)
+    nf, slots = C.c_int(0), C.c_int64(0)
+    _check(_lib.flute_plan_stream_k(tiles_m, tiles_n, tiles_k, workers, ranges, fx.ctypes.data,
+                                    cap, C.byref(nf), C.byref(slots)))
+    return StreamKPlan(ranges.reshape(-1, 2), fx[:4 * nf.value].reshape(-1, 4), slots.value)
+
+
+TRAFFIC_FIELDS = ("bytes_weights", "bytes_scales", "bytes_table", "bytes_activations",
+                  "bytes_partials_rw", "bytes_output", "flops")
+
+
+def plan_traffic(m, k, n, bits, group, layout=DEFAULT_LAYOUT, workers=1, stages=2, tile_m=0):
+    st = np.zeros(7, np.uint64)
+    _check(_lib.flute_plan_traffic(m, k, n, bits, group, _lay(layout), workers, stages, tile_m,
+                                   st))
+    return dict(zip(TRAFFIC_FIELDS, (int(v) for v in st)))
+
+
+def bits_per_param(bits: int, group: int) -> float:
+    v = _lib.flute_bits_per_param(bits, group)
+    if v < 0:
+        raise ConfigError(_lib.flute_last_error().decode())
+    return float(v)
+
+
+def algorithmic_bytes(m: int, k: int, n: int, bits: int, group: int) -> int:
+    """each byte counted once."""
+    return (k * n * bits + 7) // 8 + (k * n // group) * 2 + m * k * 2 + m * n * 2 + (1 << bits) * 2
+
+
+# --------------------------------------------------------------------------
+# device
+# --------------------------------------------------------------------------
+
+def device_count() -> int:
+    return int(_lib.flute_device_count())
+
+
+def sm_count(device: int = 0) -> int:
+    v = _lib.flute_sm_count(device)
+    if v < 0:
+        raise CudaError(_lib.flute_last_error().decode())
+    return int(v)
+
+
+def default_workers(m: int, k: int, n: int, bits: int) -> int:
+    v = _lib.flute_default_workers(m, k, n, bits)
+    if v < 0:
+        raise CudaError(_lib.flute_last_error().decode())
+    return int(v)
+
+
+def workspace_bytes(m: int, workers: int) -> int:
+    return int(_lib.flute_workspace_bytes(m, workers))
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return int(stream)
+
+
+class DeviceWeights:
+    """Device-resident quantized weights (uploaded once).  ``gemm`` is the hot
+    path: device tensors in, device tensor out, async on the current torch
+    stream.  Mirrors flutesim::DeviceWeights (include/flutesim/engine.hpp)."""
+
+    def __init__(self, indices: np.ndarray, scales: np.ndarray, table_values: np.ndarray,
+                 bits: int, group: int):
+        idx = np.ascontiguousarray(indices, np.uint8)
+        self.k, self.n = idx.shape
+        self.bits, self.group = bits, group
+        h = _vp()
+        _check(_lib.flute_weights_from_indices(idx, np.ascontiguousarray(scales, np.uint16),
+                                               np.ascontiguousarray(table_values, np.float32),
+                                               self.k, self.n, bits, group, C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_device_layout(cls, packed: np.ndarray, scales_dev: np.ndarray,
+                           vlut_words: np.ndarray, k: int, n: int, bits: int, group: int):
+        self = cls.__new__(cls)
+        self.k, self.n, self.bits, self.group = k, n, bits, group
+        h = _vp()
+        _check(_lib.flute_weights_create(np.ascontiguousarray(packed, np.uint8),
+                                         np.ascontiguousarray(scales_dev, np.uint16),
+                                         np.ascontiguousarray(vlut_words, np.uint32), k, n, bits,
+                                         group, C.byref(h)))
+        self._h = h
+        return self
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.flute_weights_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def gemm(self, x, y=None, workers: int = 0, stream=None):
+        """x: torch f16 [m][k] on cuda -> y f16 [m][n]."""
+        import torch
+        if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
+            raise InputError(f"x must be a cuda float16 [m][{self.k}] tensor")
+        x = x.contiguous()
+        m = x.shape[0]
+        if y is None:
+            y = torch.empty((m, self.n), dtype=torch.float16, device=x.device)
+        _check(_lib.flute_gemm(self._h, x.data_ptr(), m, y.data_ptr(), workers,
+                               _stream_ptr(stream)))
+        return y
+
+    def gemm_host(self, x16: np.ndarray, workers: int = 0, stream=None) -> np.ndarray:
+        """End-to-end: host f16 bits in, host f16 bits out (copies inside)."""
+        x16 = np.ascontiguousarray(x16, np.uint16)
+        m = x16.shape[0]
+        y = np.zeros((m, self.n), np.uint16)
+        _check(_lib.flute_gemm_host(self._h, x16, m, y, workers,
+                                    None if stream is None else int(stream)))
+        return y
+
+
+def qgemm(x, w_dev, scales_dev, vlut_dev, bits: int, group: int, n: int, workspace, y=None,
+          workers: int = 0, stream=None):
+    """Raw device-pointer GEMM (flute_qgemm): all arguments are torch cuda
+    tensors in the device layouts."""
+    import torch
+    m, k = x.shape
+    if y is None:
+        y = torch.empty((m, n), dtype=torch.float16, device=x.device)
+    _check(_lib.flute_qgemm(x.data_ptr(), m, k, n, w_dev.data_ptr(), scales_dev.data_ptr(),
+                            vlut_dev.data_ptr(), bits, group, y.data_ptr(), workspace.data_ptr(),
+                            workspace.numel() * workspace.element_size(), workers,
+                            _stream_ptr(stream)))
+    return y
+
+
+def dequant_all_device(vlut_words: np.ndarray, bits: int, scales: np.ndarray) -> np.ndarray:
+    """Run the GEMM kernel's own dequant routine for every pair x scale:
+    returns u32 [n_scales][2^(2b)] (reference pair order)."""
+    scales = np.ascontiguousarray(scales, np.uint16)
+    out = np.zeros((scales.size, 1 << (2 * bits)), np.uint32)
+    _check(_lib.flute_dequant_all_device(np.ascontiguousarray(vlut_words, np.uint32), bits, scales,
+                                         scales.size, out))
+    return out
+
+
+def mma_fragment(a16: np.ndarray, b16: np.ndarray, c: np.ndarray) -> np.ndarray:
+    """mma.hpp:23 on the tensor cores: returns c + a @ b (f16 in, f32 acc)."""
+    a16 = np.ascontiguousarray(a16, np.uint16)
+    b16 = np.ascontiguousarray(b16, np.uint16)
+    c = np.array(c, np.float32, copy=True, order="C")
+    m, k = a16.shape
+    n = b16.shape[1]
+    _check(_lib.flute_mma_fragment(a16, b16, c, m, n, k))
+    return c
+
+
+def exported_symbols() -> Sequence[str]:
+    return tuple(_SIGS)

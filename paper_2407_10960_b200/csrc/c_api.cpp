@@ -1,0 +1,470 @@
+// flute-b200 — C ABI implementation (include/flute_c.h).  Thin: every entry
+// point converts plain pointers to the C++ API and maps exceptions to status
+// codes, keeping the message for flute_last_error().
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "device_api.h"
+#include "flute_c.h"
+#include "flutesim/engine.hpp"
+#include "flutesim/errors.hpp"
+#include "flutesim/mma.hpp"
+
+using namespace flutesim;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return FLUTE_OK;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return FLUTE_ERR_CUDA;
+  } catch (const ConfigError& e) {
+    g_last_error = e.what();
+    return FLUTE_ERR_CONFIG;
+  } catch (const InputError& e) {
+    g_last_error = e.what();
+    return FLUTE_ERR_INPUT;
+  } catch (const InternalError& e) {
+    g_last_error = e.what();
+    return FLUTE_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FLUTE_ERR_INTERNAL;
+  }
+}
+
+LayoutDescriptor to_layout(const int* l) {
+  if (l == nullptr) return LayoutDescriptor{};
+  return LayoutDescriptor{l[0], l[1], l[2], l[3], l[4], l[5]};
+}
+
+void need(const void* p, const char* what) {
+  if (p == nullptr) throw InputError(std::string(what) + " is null");
+}
+
+PackedWeights canonical_from(const uint32_t* hi, const uint32_t* lo, int k, int n, int bits,
+                             const LayoutDescriptor& L) {
+  need(hi, "slice_hi");
+  if (bits == 3) need(lo, "slice_lo");
+  if (k < 1 || n < 1) throw ConfigError("k and n must be positive");
+  PackedWeights pw;
+  pw.layout = L;
+  pw.bits = bits;
+  pw.k = k;
+  pw.n = n;
+  const std::size_t total = static_cast<std::size_t>(k) * n;
+  if (bits == 3) {
+    pw.slices = {BitSlice{2, std::vector<uint32_t>(hi, hi + (total * 2 + 31) / 32)},
+                 BitSlice{1, std::vector<uint32_t>(lo, lo + (total + 31) / 32)}};
+  } else {
+    pw.slices = {BitSlice{bits, std::vector<uint32_t>(hi, hi + (total * bits + 31) / 32)}};
+  }
+  return pw;
+}
+
+VectorizedTable table_from_words(const uint32_t* words, int bits) {
+  need(words, "vlut_words");
+  if (bits < 2 || bits > 4) throw ConfigError("bits must be in {2,3,4}");
+  VectorizedTable vt;
+  vt.bits = bits;
+  vt.dup = 1;
+  vt.entries.resize(std::size_t{1} << (2 * bits));
+  for (std::size_t e = 0; e < vt.entries.size(); ++e) {
+    vt.entries[e] = {Half::from_bits(static_cast<uint16_t>(words[e] & 0xFFFFu)),
+                     Half::from_bits(static_cast<uint16_t>(words[e] >> 16))};
+  }
+  return vt;
+}
+
+}  // namespace
+
+struct flute_weights {
+  DeviceWeights* impl = nullptr;
+  int k = 0, n = 0, bits = 0, group = 0;
+};
+
+extern "C" {
+
+const char* flute_last_error(void) { return g_last_error.c_str(); }
+const char* flute_version(void) { return "flute-b200 0.1 (sm_100a)"; }
+
+uint16_t flute_f32_to_f16(float x) { return f32_to_f16(x).bits; }
+float flute_f16_to_f32(uint16_t h) { return f16_to_f32(Half::from_bits(h)); }
+
+int flute_nf_table(int bits, float* values_out) {
+  return guard([&] {
+    need(values_out, "values_out");
+    const LookupTable t = build_nf_table(bits);
+    std::memcpy(values_out, t.values.data(), t.values.size() * sizeof(float));
+  });
+}
+
+int flute_quantize(const float* w, int k, int n, int bits, int group, uint8_t* indices_out,
+                   uint16_t* scales_out) {
+  return guard([&] {
+    need(w, "w");
+    need(indices_out, "indices_out");
+    need(scales_out, "scales_out");
+    if (k < 1 || n < 1) throw ConfigError("k and n must be positive");
+    MatF m(k, n);
+    std::memcpy(m.data.data(), w, sizeof(float) * m.data.size());
+    const QuantizedMatrix q = quantize_matrix(m, QuantConfig{bits, group});
+    std::memcpy(indices_out, q.indices.data(), q.indices.size());
+    for (std::size_t i = 0; i < q.scales.size(); ++i) scales_out[i] = q.scales[i].bits;
+  });
+}
+
+size_t flute_canonical_words(int k, int n, int slice_bits) {
+  return (static_cast<size_t>(k) * n * slice_bits + 31) / 32;
+}
+
+int flute_pack_canonical(const uint8_t* indices, int k, int n, int bits, const int* layout,
+                         uint32_t* slice_hi, uint32_t* slice_lo) {
+  return guard([&] {
+    need(indices, "indices");
+    need(slice_hi, "slice_hi");
+    if (bits == 3) need(slice_lo, "slice_lo");
+    QuantizedMatrix q;
+    q.cfg.bits = bits;
+    q.k = k;
+    q.n = n;
+    if (bits < 2 || bits > 4) throw ConfigError("bits must be in {2,3,4}");
+    q.indices.assign(indices, indices + static_cast<size_t>(k) * n);
+    const PackedWeights pw = reorder_and_split(q, to_layout(layout));
+    std::memcpy(slice_hi, pw.slices[0].words.data(), pw.slices[0].words.size() * 4);
+    if (bits == 3) std::memcpy(slice_lo, pw.slices[1].words.data(), pw.slices[1].words.size() * 4);
+  });
+}
+
+int flute_unpack_canonical(const uint32_t* slice_hi, const uint32_t* slice_lo, int k, int n,
+                           int bits, const int* layout, uint8_t* indices_out) {
+  return guard([&] {
+    need(indices_out, "indices_out");
+    const LayoutDescriptor L = to_layout(layout);
+    L.validate();
+    const std::vector<uint8_t> idx = unpack_matrix(canonical_from(slice_hi, slice_lo, k, n, bits, L));
+    std::memcpy(indices_out, idx.data(), idx.size());
+  });
+}
+
+int flute_device_sizes(int k, int n, int bits, int group, size_t* weight_bytes,
+                       size_t* scale_bytes) {
+  return guard([&] {
+    const DeviceGeometry g = device_geometry(k, n, bits, group);
+    if (weight_bytes) *weight_bytes = g.weight_bytes();
+    if (scale_bytes) *scale_bytes = g.scale_bytes();
+  });
+}
+
+int flute_pack_device(const uint8_t* indices, int k, int n, int bits, int group, uint8_t* out) {
+  return guard([&] {
+    need(indices, "indices");
+    need(out, "out");
+    const std::vector<uint8_t> idx(indices, indices + static_cast<size_t>(k) * n);
+    const std::vector<uint8_t> dev = pack_device(idx, k, n, bits, group);
+    std::memcpy(out, dev.data(), dev.size());
+  });
+}
+
+int flute_repack_canonical(const uint32_t* slice_hi, const uint32_t* slice_lo, int k, int n,
+                           int bits, const int* layout, int group, uint8_t* out) {
+  return guard([&] {
+    need(out, "out");
+    const LayoutDescriptor L = to_layout(layout);
+    L.validate();
+    const std::vector<uint8_t> dev =
+        pack_device_from_canonical(canonical_from(slice_hi, slice_lo, k, n, bits, L), group);
+    std::memcpy(out, dev.data(), dev.size());
+  });
+}
+
+int flute_unpack_device(const uint8_t* packed, int k, int n, int bits, int group,
+                        uint8_t* indices_out) {
+  return guard([&] {
+    need(packed, "packed");
+    need(indices_out, "indices_out");
+    const DeviceGeometry g = device_geometry(k, n, bits, group);
+    const std::vector<uint8_t> dev(packed, packed + g.weight_bytes());
+    const std::vector<uint8_t> idx = unpack_device(dev, k, n, bits, group);
+    std::memcpy(indices_out, idx.data(), idx.size());
+  });
+}
+
+int flute_scales_device(const uint16_t* scales, int k, int n, int group, uint16_t* out) {
+  return guard([&] {
+    need(scales, "scales");
+    need(out, "out");
+    QuantConfig{4, group}.validate(k);
+    std::vector<Half> s(static_cast<size_t>(k / group) * n);
+    for (size_t i = 0; i < s.size(); ++i) s[i] = Half::from_bits(scales[i]);
+    const std::vector<uint16_t> d = scales_to_device(s, k, n, group);
+    std::memcpy(out, d.data(), d.size() * 2);
+  });
+}
+
+int flute_vlut_build(const float* table_values, int bits, int dup, uint32_t* out) {
+  return guard([&] {
+    need(table_values, "table_values");
+    need(out, "out");
+    LookupTable t;
+    t.bits = bits;
+    if (bits < 1 || bits > 4) throw ConfigError("bits must be in {2,3,4}");
+    t.values.assign(table_values, table_values + (1 << bits));
+    const VectorizedTable vt = make_vectorized_lut(t, dup);
+    for (std::size_t e = 0; e < vt.entries.size(); ++e) {
+      const uint32_t wv = static_cast<uint32_t>(vt.entries[e].first.bits) |
+                          (static_cast<uint32_t>(vt.entries[e].second.bits) << 16);
+      for (int c = 0; c < dup; ++c) out[vt.address(static_cast<uint32_t>(e), c)] = wv;
+    }
+  });
+}
+
+int flute_vlut_device_words(const uint32_t* vlut_words, int bits, uint32_t* out) {
+  return guard([&] {
+    need(out, "out");
+    const std::vector<uint32_t> d = device_vlut_words(table_from_words(vlut_words, bits));
+    std::memcpy(out, d.data(), d.size() * 4);
+  });
+}
+
+int flute_vec_dequantize(uint32_t pair, uint16_t scale, const uint32_t* vlut_words, int bits,
+                         uint32_t* out) {
+  return guard([&] {
+    need(out, "out");
+    const auto r = vec_dequantize(pair, Half::from_bits(scale), table_from_words(vlut_words, bits));
+    *out = static_cast<uint32_t>(r.first.bits) | (static_cast<uint32_t>(r.second.bits) << 16);
+  });
+}
+
+int flute_plan_stream_k(int tiles_m, int tiles_n, int tiles_k, int workers, int64_t* ranges,
+                        int64_t* fixups, int max_fixups, int* n_fixups, int64_t* total_slots) {
+  return guard([&] {
+    need(ranges, "ranges");
+    const StreamKPlan p = plan_stream_k(TileGrid{tiles_m, tiles_n, tiles_k}, workers);
+    for (int w = 0; w < workers; ++w) {
+      ranges[2 * w] = p.ranges[w].begin;
+      ranges[2 * w + 1] = p.ranges[w].end;
+    }
+    if (n_fixups) *n_fixups = static_cast<int>(p.fixups.size());
+    if (total_slots) *total_slots = p.total_slots;
+    if (fixups) {
+      for (int f = 0; f < static_cast<int>(p.fixups.size()) && f < max_fixups; ++f) {
+        fixups[4 * f] = p.fixups[f].tile;
+        fixups[4 * f + 1] = p.fixups[f].finisher;
+        fixups[4 * f + 2] = p.fixups[f].slot_base;
+        fixups[4 * f + 3] = static_cast<int64_t>(p.fixups[f].contributors.size());
+      }
+    }
+  });
+}
+
+int flute_plan_traffic(int m, int k, int n, int bits, int group, const int* layout, int workers,
+                       int stages, int tile_m, uint64_t* stats) {
+  return guard([&] {
+    need(stats, "stats");
+    ProblemShape s;
+    s.m = m;
+    s.k = k;
+    s.n = n;
+    s.cfg = QuantConfig{bits, group};
+    s.layout = to_layout(layout);
+    s.workers = workers;
+    s.stages = stages;
+    s.tile_m = tile_m;
+    const TrafficStats t = plan_traffic(s);
+    const uint64_t v[7] = {t.bytes_weights,     t.bytes_scales, t.bytes_table, t.bytes_activations,
+                           t.bytes_partials_rw, t.bytes_output, t.flops};
+    std::memcpy(stats, v, sizeof(v));
+  });
+}
+
+double flute_bits_per_param(int bits, int group) {
+  try {
+    return bits_per_param(QuantConfig{bits, group});
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return -1.0;
+  }
+}
+
+int flute_device_count(void) { return flute_dev::device_count(); }
+
+int flute_sm_count(int device) {
+  int v = 0;
+  if (guard([&] { v = flute_dev::sm_count(device); }) != FLUTE_OK) return -1;
+  return v;
+}
+
+int flute_max_workers(int m) {
+  int v = -1;
+  if (guard([&] { v = flute_dev::max_workers(m); }) != FLUTE_OK) return -1;
+  return v;
+}
+
+int flute_default_workers(int m, int k, int n, int bits) {
+  int v = -1;
+  if (guard([&] { v = flute_dev::default_workers(m, k, n, bits); }) != FLUTE_OK) return -1;
+  return v;
+}
+
+size_t flute_workspace_bytes(int m, int workers) { return flute_dev::workspace_bytes(m, workers); }
+
+int flute_qgemm(const void* x, int m, int k, int n, const void* w, const void* scales,
+                const void* vlut, int bits, int group, void* y, void* workspace,
+                size_t workspace_bytes, int workers, void* stream) {
+  return guard([&] {
+    QuantConfig{bits, group}.validate(k);
+    flute_dev::GemmArgs a;
+    a.x = x;
+    a.m = m;
+    a.k = k;
+    a.n = n;
+    a.w = w;
+    a.scales = scales;
+    a.vlut = vlut;
+    a.bits = bits;
+    a.group = group;
+    a.y = y;
+    a.workspace = workspace;
+    a.workspace_bytes = workspace_bytes;
+    a.workers = workers;
+    a.stream = stream;
+    flute_dev::qgemm(a);
+  });
+}
+
+int flute_weights_create(const uint8_t* packed_host, const uint16_t* scales_dev_layout_host,
+                         const uint32_t* vlut_words, int k, int n, int bits, int group,
+                         flute_weights** out) {
+  return guard([&] {
+    need(packed_host, "packed_host");
+    need(scales_dev_layout_host, "scales");
+    need(out, "out");
+    const DeviceGeometry g = device_geometry(k, n, bits, group);
+    // Recover indices + [n][k/g] scales from the device layouts, then reuse
+    // the DeviceWeights constructor (keeps one upload path).
+    const std::vector<uint8_t> idx =
+        unpack_device(std::vector<uint8_t>(packed_host, packed_host + g.weight_bytes()), k, n, bits, group);
+    const int gpc = k / group, gp = g.groups_padded();
+    std::vector<Half> sc(static_cast<size_t>(gpc) * n);
+    for (int col = 0; col < n; ++col) {
+      const int nt = col / kUnitN, c = col % kUnitN;
+      const int j = c / 16, gr = c % 8, h = (c % 16) / 8;
+      for (int G = 0; G < gpc; ++G)
+        sc[static_cast<size_t>(col) * gpc + G] = Half::from_bits(
+            scales_dev_layout_host[(static_cast<size_t>(nt) * gp + G) * kUnitN + gr * 8 + j * 2 + h]);
+    }
+    const VectorizedTable vt = table_from_words(vlut_words, bits);
+    LookupTable t;
+    t.bits = bits;
+    for (int i = 0; i < (1 << bits); ++i) t.values.push_back(f16_to_f32(vt.entries[static_cast<size_t>(i) << bits].first));
+    auto* h = new flute_weights;
+    h->impl = new DeviceWeights(idx, sc, t, k, n, QuantConfig{bits, group});
+    h->k = k;
+    h->n = n;
+    h->bits = bits;
+    h->group = group;
+    *out = h;
+  });
+}
+
+int flute_weights_from_indices(const uint8_t* indices, const uint16_t* scales,
+                               const float* table_values, int k, int n, int bits, int group,
+                               flute_weights** out) {
+  return guard([&] {
+    need(indices, "indices");
+    need(scales, "scales");
+    need(table_values, "table_values");
+    need(out, "out");
+    QuantConfig{bits, group}.validate(k);
+    std::vector<Half> sc(static_cast<size_t>(k / group) * n);
+    for (size_t i = 0; i < sc.size(); ++i) sc[i] = Half::from_bits(scales[i]);
+    LookupTable t;
+    t.bits = bits;
+    t.values.assign(table_values, table_values + (1 << bits));
+    auto* h = new flute_weights;
+    try {
+      h->impl = new DeviceWeights(std::vector<uint8_t>(indices, indices + static_cast<size_t>(k) * n),
+                                  sc, t, k, n, QuantConfig{bits, group});
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    h->k = k;
+    h->n = n;
+    h->bits = bits;
+    h->group = group;
+    *out = h;
+  });
+}
+
+int flute_weights_destroy(flute_weights* w) {
+  return guard([&] {
+    if (w == nullptr) return;
+    delete w->impl;
+    delete w;
+  });
+}
+
+int flute_weights_info(const flute_weights* w, int* k, int* n, int* bits, int* group) {
+  return guard([&] {
+    need(w, "weights");
+    if (k) *k = w->k;
+    if (n) *n = w->n;
+    if (bits) *bits = w->bits;
+    if (group) *group = w->group;
+  });
+}
+
+int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int workers,
+               void* stream) {
+  return guard([&] {
+    need(w, "weights");
+    w->impl->gemm(static_cast<const Half*>(x_dev), m, static_cast<Half*>(y_dev), workers, stream);
+  });
+}
+
+int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
+                    int workers, void* stream) {
+  return guard([&] {
+    need(w, "weights");
+    need(x_host, "x_host");
+    need(y_host, "y_host");
+    MatH x(m, w->k);
+    for (size_t i = 0; i < x.data.size(); ++i) x.data[i] = Half::from_bits(x_host[i]);
+    const MatH y = w->impl->gemm_host(x, workers, stream);
+    for (size_t i = 0; i < y.data.size(); ++i) y_host[i] = y.data[i].bits;
+  });
+}
+
+int flute_dequant_all_device(const uint32_t* vlut_words, int bits, const uint16_t* scales,
+                             int n_scales, uint32_t* out_host) {
+  return guard([&] {
+    need(scales, "scales");
+    need(out_host, "out_host");
+    const std::vector<uint32_t> d = device_vlut_words(table_from_words(vlut_words, bits));
+    flute_dev::dequant_all(d.data(), bits, scales, n_scales, out_host);
+  });
+}
+
+int flute_mma_fragment(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(c, "c");
+    FragDims d{m, n, k};
+    mma_fragment(std::span<const Half>(reinterpret_cast<const Half*>(a), static_cast<size_t>(m) * k),
+                 std::span<const Half>(reinterpret_cast<const Half*>(b), static_cast<size_t>(k) * n),
+                 std::span<float>(c, static_cast<size_t>(m) * n), d);
+  });
+}
+
+}  // extern "C"

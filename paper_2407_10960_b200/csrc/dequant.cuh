@@ -1,0 +1,97 @@
+// flute-b200 — register-level LUT dequantization (FLUTE §3.2, Alg. 1 "vectorized
+// lookup"; reference semantics vec_lut.cpp:39-48).
+//
+// Shared-memory vLUT: entry e occupies one 256-byte row; lane l reads its own
+// copy at e*256 + 4l, so a warp's 32 lookups always hit 32 distinct banks
+// (duplication 32, conflict-free).  The byte offset e*256 + 4l is produced by a
+// single PRMT from a byte vector of device pair indices (byte p -> bits 8..15,
+// lane*4 -> bits 0..7), which ptxas folds into LDS [R + UR + imm].
+//
+// Dequant: half2 = vLUT[e] * (s, s) with one HMUL2 (mul.rn.f16x2).  The product
+// of two binary16 values is exact in binary32, so f16(f32(s) * f32(T)) — the
+// reference rule — equals the RNE f16x2 product bit for bit (subnormals are
+// kept by f16 arithmetic on sm_100).
+//
+// Per lane and 16-deep k step, the device layout (host_pack.cpp) gives 16 pair
+// indices q = 4j + p (atom j = 16-column block, p = A-fragment register):
+//   4-bit: uint4, byte p of word j = pair 4j+p                      (8 bits/pair)
+//   2-bit: uint2, word h: low nibbles of bytes 0..3 = pairs 8h+0..3, high
+//          nibbles = pairs 8h+4..7                                   (4 bits/pair)
+//   3-bit: same nibble layout for the hi plane (hi_k<<2 | hi_k1), plus one u32
+//          lo word: bits 2c..2c+1 of byte b = lo pair (lo_k<<1 | lo_k1) of
+//          pair 4c+b.  Device index = (hi_nibble << 2) | lo2.
+#pragma once
+
+#include "ptx.cuh"
+
+namespace flute_dev {
+
+inline constexpr int kLutRowBytes = 256;
+
+template <int BITS>
+struct LaneBits;
+template <>
+struct LaneBits<4> {
+  uint4 w;
+};
+template <>
+struct LaneBits<2> {
+  uint2 w;
+};
+template <>
+struct LaneBits<3> {
+  uint2 hi;
+  uint32_t lo;
+};
+
+// Byte vector of the 4 device pair indices of atom j (byte p = register p).
+template <int BITS>
+__device__ __forceinline__ uint32_t atom_index_bytes(const LaneBits<BITS>& lb, int j);
+
+template <>
+__device__ __forceinline__ uint32_t atom_index_bytes<4>(const LaneBits<4>& lb, int j) {
+  return j == 0 ? lb.w.x : j == 1 ? lb.w.y : j == 2 ? lb.w.z : lb.w.w;
+}
+template <>
+__device__ __forceinline__ uint32_t atom_index_bytes<2>(const LaneBits<2>& lb, int j) {
+  const uint32_t w = (j >> 1) ? lb.w.y : lb.w.x;
+  return (j & 1) ? ((w >> 4) & 0x0F0F0F0Fu) : (w & 0x0F0F0F0Fu);
+}
+template <>
+__device__ __forceinline__ uint32_t atom_index_bytes<3>(const LaneBits<3>& lb, int j) {
+  const uint32_t w = (j >> 1) ? lb.hi.y : lb.hi.x;
+  const uint32_t hi = (j & 1) ? ((w >> 2) & 0x3C3C3C3Cu) : ((w << 2) & 0x3C3C3C3Cu);
+  return hi | ((lb.lo >> (2 * j)) & 0x03030303u);
+}
+
+// The four A-fragment registers of atom j: a[p] = vLUT[idx_p] * scale2(p),
+// with regs 0/2 (column g) scaled by s_lo and regs 1/3 (column g+8) by s_hi.
+__device__ __forceinline__ void lut_dequant4(uint32_t idx_bytes, uint32_t lane4, uint32_t lut_base,
+                                             uint32_t s_lo, uint32_t s_hi, uint32_t (&a)[4]) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t off = prmt(idx_bytes, lane4, 0x5504u | (static_cast<uint32_t>(p) << 4));
+    const uint32_t v = lds32(lut_base + off);
+    a[p] = hmul2_u32(v, (p & 1) ? s_hi : s_lo);
+  }
+}
+
+// Expand the 2^(2b) device-order vLUT words into the 32-copy shared table.
+// Called by `nthreads` threads with ids [0, nthreads).
+template <int BITS>
+__device__ __forceinline__ void fill_lut(uint32_t lut_base, const uint32_t* __restrict__ vlut,
+                                         int tid, int nthreads) {
+  constexpr int kEntries = 1 << (2 * BITS);
+  // Each row: 8 x 16-byte chunks hold the 32 lane copies (bytes 0..127).
+  for (int c = tid; c < kEntries * 8; c += nthreads) {
+    const int e = c >> 3;
+    const uint32_t v = __ldg(vlut + e);
+    sts128(lut_base + e * kLutRowBytes + (c & 7) * 16, make_uint4(v, v, v, v));
+  }
+}
+
+// Broadcast the halves of a packed scale word: (lo, lo) and (hi, hi).
+__device__ __forceinline__ uint32_t dup_lo(uint32_t s) { return prmt(s, s, 0x1010u); }
+__device__ __forceinline__ uint32_t dup_hi(uint32_t s) { return prmt(s, s, 0x3232u); }
+
+}  // namespace flute_dev

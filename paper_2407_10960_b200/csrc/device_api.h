@@ -1,0 +1,45 @@
+// flute-b200 — internal interface between the C++ host layer and the CUDA
+// translation units.  No CUDA types: streams are void* (cudaStream_t).
+// Every function throws flutesim::{ConfigError, InputError, CudaError}.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace flute_dev {
+
+struct GemmArgs {
+  const void* x = nullptr;       // f16 [m][k], device
+  int m = 0, k = 0, n = 0;
+  const void* w = nullptr;       // device-layout weights, device
+  const void* scales = nullptr;  // device-layout scales, device
+  const void* vlut = nullptr;    // 2^(2b) device-order u32 words, device
+  int bits = 4, group = 128;
+  void* y = nullptr;             // f16 [m][n], device
+  void* workspace = nullptr;
+  std::size_t workspace_bytes = 0;
+  int workers = 0;               // <= 0: default
+  void* stream = nullptr;
+};
+
+void qgemm(const GemmArgs& a);
+std::size_t workspace_bytes(int m, int workers);
+int max_workers(int m);
+int default_workers(int m, int k, int n, int bits);
+int sm_count(int device);
+int device_count();
+
+// Device self-checks.
+void dequant_all(const std::uint32_t* vlut_dev_words_host, int bits, const std::uint16_t* scales,
+                 int n_scales, std::uint32_t* out_host);
+void mma_fragment(const std::uint16_t* a, const std::uint16_t* b, float* c, int m, int n, int k);
+
+// Small RAII device buffer helpers used by the host layer.
+void* dev_alloc(std::size_t bytes);
+void dev_free(void* p);
+void h2d(void* dst, const void* src, std::size_t bytes, void* stream);
+void d2h(void* dst, const void* src, std::size_t bytes, void* stream);
+void dev_zero(void* p, std::size_t bytes, void* stream);
+void stream_sync(void* stream);
+
+}  // namespace flute_dev

@@ -1,0 +1,286 @@
+// flute-b200 — host engine: the drop-in execute() (reference engine.cpp:345),
+// the reference traffic model (engine.cpp:87-130, 375-418) and the
+// device-resident weight handle.  All compute goes to the GPU kernel through
+// flute_dev::qgemm; there is no CPU fallback.
+#include <algorithm>
+#include <string>
+
+#include "device_api.h"
+#include "flutesim/engine.hpp"
+#include "flutesim/errors.hpp"
+#include "flutesim/mma.hpp"
+
+namespace flutesim {
+
+TrafficStats& TrafficStats::operator+=(const TrafficStats& o) {
+  bytes_weights += o.bytes_weights;
+  bytes_scales += o.bytes_scales;
+  bytes_table += o.bytes_table;
+  bytes_activations += o.bytes_activations;
+  bytes_partials_rw += o.bytes_partials_rw;
+  bytes_output += o.bytes_output;
+  flops += o.flops;
+  return *this;
+}
+
+namespace {
+
+struct Shape {
+  int m = 0, k = 0, n = 0, tile_m = 0;
+  LayoutDescriptor L;
+  QuantConfig cfg;
+  TileGrid grid;
+};
+
+// engine.cpp:59-85 validation order and messages.
+Shape make_shape(int m, int k, int n, const LayoutDescriptor& L, const QuantConfig& cfg,
+                 int tile_m_override, int stages, int workers) {
+  L.validate();
+  cfg.validate(k);
+  Shape s;
+  s.m = m;
+  s.k = k;
+  s.n = n;
+  s.L = L;
+  s.cfg = cfg;
+  s.tile_m = tile_m_override > 0 ? tile_m_override : L.tile_m;
+  if (m < 1) throw ConfigError("matmul: m must be >= 1");
+  if (workers < 1) throw ConfigError("matmul: workers must be >= 1");
+  if (stages < 1) throw ConfigError("matmul: pipeline stages must be >= 1");
+  if (s.tile_m % L.frag_m != 0) throw ConfigError("matmul: tile_m must divide by frag_m");
+  if (k % L.tile_k != 0 || n % L.tile_n != 0) throw ConfigError("matmul: dims must divide by tile dims");
+  s.grid = TileGrid{(m + s.tile_m - 1) / s.tile_m, n / L.tile_n, k / L.tile_k};
+  return s;
+}
+
+int rows_in(const Shape& s, long mt) {
+  return static_cast<int>(std::min<long>(s.tile_m, static_cast<long>(s.m) - mt * s.tile_m));
+}
+
+// The reference's per-worker accounting: every unit of a non-empty range is
+// fetched once (activations, weights, scales), the table once per worker,
+// partial tiles written by contributors and read by finishers, outputs once.
+TrafficStats account(const Shape& s, int workers) {
+  const StreamKPlan plan = plan_stream_k(s.grid, workers);
+  const LayoutDescriptor& L = s.L;
+  const std::uint64_t tile_bytes = static_cast<std::uint64_t>(s.tile_m) * L.tile_n * 2;
+  const std::uint64_t unit_flops = static_cast<std::uint64_t>(s.tile_m / L.frag_m) *
+                                   L.frags_per_tile_n() * L.frags_per_tile_k() * 2ull * L.frag_m *
+                                   L.frag_n * L.frag_k;
+  const std::uint64_t weight_tile = static_cast<std::uint64_t>(L.tile_elems()) * s.cfg.bits / 8;
+  TrafficStats t;
+  for (int w = 0; w < workers; ++w) {
+    const WorkerRange r = plan.ranges[w];
+    if (r.size() == 0) continue;
+    t.bytes_table += (std::uint64_t{1} << (2 * s.cfg.bits)) * 4;
+    for (long u = r.begin; u < r.end; ++u) {
+      const long tile = u / s.grid.tiles_k;
+      const long mt = tile / s.grid.tiles_n;
+      const long kt = u % s.grid.tiles_k;
+      t.bytes_activations += static_cast<std::uint64_t>(rows_in(s, mt)) * L.tile_k * 2;
+      t.bytes_weights += weight_tile;
+      const long k0 = kt * L.tile_k, k1 = k0 + L.tile_k - 1;
+      t.bytes_scales +=
+          static_cast<std::uint64_t>((k1 / s.cfg.group_size - k0 / s.cfg.group_size + 1) * L.tile_n) * 2;
+      t.flops += unit_flops;
+      const bool tile_end = u + 1 >= r.end || (u + 1) % s.grid.tiles_k == 0;
+      if (!tile_end) continue;
+      const bool finished = r.end >= (tile + 1) * s.grid.tiles_k;
+      const bool started = r.begin <= tile * s.grid.tiles_k;
+      if (!finished) {
+        t.bytes_partials_rw += tile_bytes;
+        continue;
+      }
+      if (!started) {
+        t.bytes_partials_rw += tile_bytes * plan.fixup_for(tile)->contributors.size();
+      }
+      t.bytes_output += static_cast<std::uint64_t>(rows_in(s, mt)) * L.tile_n * 2;
+    }
+  }
+  return t;
+}
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  std::size_t bytes = 0;
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t n) : p(flute_dev::dev_alloc(n)), bytes(n) {}
+  ~DeviceBuffer() { flute_dev::dev_free(p); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    return *this;
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// DeviceWeights
+// ---------------------------------------------------------------------------
+
+struct DeviceWeights::Impl {
+  int k = 0, n = 0, bits = 0, group = 0;
+  DeviceBuffer w, sc, lut, ws, xbuf, ybuf;
+
+  void upload(const std::vector<std::uint8_t>& packed, const std::vector<std::uint16_t>& scales,
+              const std::vector<std::uint32_t>& lut_words) {
+    w = DeviceBuffer(packed.size());
+    sc = DeviceBuffer(scales.size() * 2);
+    lut = DeviceBuffer(lut_words.size() * 4);
+    flute_dev::h2d(w.p, packed.data(), packed.size(), nullptr);
+    flute_dev::h2d(sc.p, scales.data(), scales.size() * 2, nullptr);
+    flute_dev::h2d(lut.p, lut_words.data(), lut_words.size() * 4, nullptr);
+    const int maxw = std::max(flute_dev::max_workers(32), 1) * 4;  // ticket mode headroom
+    ws = DeviceBuffer(flute_dev::workspace_bytes(32, maxw));
+    flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
+    flute_dev::stream_sync(nullptr);
+  }
+
+  void gemm(const void* x, int m, void* y, int workers, void* stream) {
+    if (workers > 0 && flute_dev::workspace_bytes(m, workers) > ws.bytes) {
+      ws = DeviceBuffer(flute_dev::workspace_bytes(m, workers));
+      flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
+      flute_dev::stream_sync(nullptr);
+    }
+    flute_dev::GemmArgs a;
+    a.x = x;
+    a.m = m;
+    a.k = k;
+    a.n = n;
+    a.w = w.p;
+    a.scales = sc.p;
+    a.vlut = lut.p;
+    a.bits = bits;
+    a.group = group;
+    a.y = y;
+    a.workspace = ws.p;
+    a.workspace_bytes = ws.bytes;
+    a.workers = workers;
+    a.stream = stream;
+    flute_dev::qgemm(a);
+  }
+};
+
+DeviceWeights::DeviceWeights(const PackedWeights& pw, const std::vector<Half>& scales,
+                             const VectorizedTable& lut, const QuantConfig& cfg)
+    : impl_(std::make_unique<Impl>()) {
+  cfg.validate(pw.k);
+  if (pw.bits != cfg.bits || lut.bits != cfg.bits) {
+    throw ConfigError("device weights: bit width mismatch between config, weights, and table");
+  }
+  impl_->k = pw.k;
+  impl_->n = pw.n;
+  impl_->bits = pw.bits;
+  impl_->group = cfg.group_size;
+  impl_->upload(pack_device_from_canonical(pw, cfg.group_size),
+                scales_to_device(scales, pw.k, pw.n, cfg.group_size), device_vlut_words(lut));
+}
+
+DeviceWeights::DeviceWeights(const std::vector<std::uint8_t>& indices,
+                             const std::vector<Half>& scales, const LookupTable& table, int k,
+                             int n, const QuantConfig& cfg)
+    : impl_(std::make_unique<Impl>()) {
+  cfg.validate(k);
+  if (table.bits != cfg.bits) throw ConfigError("device weights: table bit width mismatch");
+  impl_->k = k;
+  impl_->n = n;
+  impl_->bits = cfg.bits;
+  impl_->group = cfg.group_size;
+  impl_->upload(pack_device(indices, k, n, cfg.bits, cfg.group_size),
+                scales_to_device(scales, k, n, cfg.group_size),
+                device_vlut_words(make_vectorized_lut(table, 1)));
+}
+
+DeviceWeights::~DeviceWeights() = default;
+int DeviceWeights::k() const { return impl_->k; }
+int DeviceWeights::n() const { return impl_->n; }
+
+void DeviceWeights::gemm(const Half* x_dev, int m, Half* y_dev, int workers, void* stream) {
+  impl_->gemm(x_dev, m, y_dev, workers, stream);
+}
+
+MatH DeviceWeights::gemm_host(const MatH& x, int workers, void* stream) {
+  if (x.cols != impl_->k) throw ConfigError("gemm_host: activation K does not match weight K");
+  const std::size_t xb = x.data.size() * 2;
+  const std::size_t yb = static_cast<std::size_t>(x.rows) * impl_->n * 2;
+  if (impl_->xbuf.bytes < xb) impl_->xbuf = DeviceBuffer(xb);
+  if (impl_->ybuf.bytes < yb) impl_->ybuf = DeviceBuffer(yb);
+  MatH y(x.rows, impl_->n);
+  flute_dev::h2d(impl_->xbuf.p, x.data.data(), xb, stream);
+  impl_->gemm(impl_->xbuf.p, x.rows, impl_->ybuf.p, workers, stream);
+  flute_dev::d2h(y.data.data(), impl_->ybuf.p, yb, stream);
+  flute_dev::stream_sync(stream);
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// Reference API
+// ---------------------------------------------------------------------------
+
+MatmulResult execute(const MatmulProblem& problem) {
+  if (problem.x == nullptr || problem.weights == nullptr || problem.scales == nullptr ||
+      problem.lut == nullptr) {
+    throw InputError("matmul: problem is missing inputs");
+  }
+  const PackedWeights& pw = *problem.weights;
+  if (problem.x->cols != pw.k) {
+    throw ConfigError("matmul: activation K (" + std::to_string(problem.x->cols) +
+                      ") does not match weight K (" + std::to_string(pw.k) + ")");
+  }
+  if (problem.cfg.bits != pw.bits || problem.lut->bits != pw.bits) {
+    throw ConfigError("matmul: bit width mismatch between config, weights, and table");
+  }
+  const long expected = static_cast<long>(pw.k) * pw.n / problem.cfg.group_size;
+  if (static_cast<long>(problem.scales->size()) != expected) {
+    throw InputError("matmul: expected " + std::to_string(expected) + " scales, got " +
+                     std::to_string(problem.scales->size()));
+  }
+  const Shape s = make_shape(problem.x->rows, pw.k, pw.n, pw.layout, problem.cfg, problem.tile_m,
+                             problem.stages, problem.workers);
+  DeviceWeights dw(pw, *problem.scales, *problem.lut, problem.cfg);
+  MatmulResult r;
+  r.y = dw.gemm_host(*problem.x, problem.workers, nullptr);
+  r.stats = account(s, problem.workers);
+  return r;
+}
+
+double bits_per_param(const QuantConfig& cfg) {
+  cfg.validate();
+  return cfg.bits + 16.0 / cfg.group_size;
+}
+
+double weight_traffic_ratio(const TrafficStats& stats, double dense_weight_bytes) {
+  if (dense_weight_bytes <= 0.0) {
+    throw InputError("weight_traffic_ratio: dense byte count must be positive");
+  }
+  return static_cast<double>(stats.bytes_weights + stats.bytes_scales) / dense_weight_bytes;
+}
+
+TrafficStats plan_traffic(const ProblemShape& shape) {
+  const Shape s = make_shape(shape.m, shape.k, shape.n, shape.layout, shape.cfg, shape.tile_m,
+                             shape.stages, shape.workers);
+  return account(s, shape.workers);
+}
+
+void mma_fragment(std::span<const Half> a, std::span<const Half> b, std::span<float> c,
+                  const FragDims& dims) {
+  const auto m = static_cast<std::size_t>(dims.m), n = static_cast<std::size_t>(dims.n),
+             k = static_cast<std::size_t>(dims.k);
+  if (dims.m <= 0 || dims.n <= 0 || dims.k <= 0 || a.size() != m * k || b.size() != k * n ||
+      c.size() != m * n) {
+    throw ConfigError("mma_fragment: fragment shape mismatch (m=" + std::to_string(dims.m) +
+                      " n=" + std::to_string(dims.n) + " k=" + std::to_string(dims.k) + ")");
+  }
+  flute_dev::mma_fragment(reinterpret_cast<const std::uint16_t*>(a.data()),
+                          reinterpret_cast<const std::uint16_t*>(b.data()), c.data(), dims.m,
+                          dims.n, dims.k);
+}
+
+}  // namespace flutesim

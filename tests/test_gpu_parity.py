@@ -1,0 +1,242 @@
+"""GPU parity: the product CUDA path (through the C ABI) vs the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * dequantized LUT values: bit-exact vs vec_dequantize (vec_lut.cpp:39-48),
+    exhaustively over every pair and every finite binary16 scale;
+  * GEMM: |y - y64| <= 1e-2 * max(|y64|, rms(y64)) per element, y64 = binary64
+    product over the f16-rounded dequantized weights; and the
+    same bound against the reference engine's own output y_ref;
+  * determinism and the reference's bitwise contracts (test_engine.cpp:162-206).
+"""
+import numpy as np
+import pytest
+
+from conftest import f16_bits
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # relative, fp16 output (north_star)
+
+
+def _case(F, orc, rng, m, k, n, bits, group, x_scale=0.5):
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    idx, scales = F.quantize_matrix(w, bits, group)
+    table = F.build_nf_table(bits)
+    x16 = f16_bits(orc, rng.standard_normal((m, k)) * x_scale)
+    return idx, scales, table, x16
+
+
+def _within(y16, y64, tol=TOL):
+    y = y16.view(np.float16).astype(np.float64)
+    bound = tol * np.maximum(np.abs(y64), np.sqrt(np.mean(y64 ** 2)) + 1e-30)
+    err = np.abs(y - y64)
+    return bool(np.all(err <= bound)), float(err.max()), float((err / bound).max())
+
+
+def _gemm(F, gpu, idx, scales, table, x16, bits, group, workers=0):
+    dw = F.DeviceWeights(idx, scales, table, bits, group)
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    y = dw.gemm(x, workers=workers)
+    gpu.cuda.synchronize()
+    return y.cpu().numpy().view(np.uint16), dw
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_dequant_bit_exact_all_pairs_all_scales(F, orc, gpu, bits):
+    """Every device-dequantized half2 == vec_dequantize, for all 2^(2b) pairs
+    and all 63488 finite binary16 scales (incl. subnormals and negatives)."""
+    table = F.build_nf_table(bits)
+    vlut = F.make_vectorized_lut(table, bits)
+    allh = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    finite = allh[(allh & 0x7C00) != 0x7C00]
+    dev = F.dequant_all_device(vlut, bits, finite)
+    want = orc.dequant_table(vlut, bits, finite)
+    mism = np.count_nonzero(dev != want)
+    assert mism == 0, f"{mism} mismatching half2 lookups"
+
+
+def test_dequant_arbitrary_table(F, orc, gpu):
+    """Any LUT (not just NF) — random f16 table values incl. subnormals."""
+    rng = np.random.default_rng(5)
+    for bits in (2, 3, 4):
+        vals = np.sort(rng.standard_normal(1 << bits).astype(np.float32) * 3)
+        vals[0] = 3e-6  # subnormal in f16
+        vlut = F.make_vectorized_lut(vals, bits)
+        sc = f16_bits(orc, rng.uniform(-8, 8, 4096))
+        assert np.array_equal(F.dequant_all_device(vlut, bits, sc), orc.dequant_table(vlut, bits, sc))
+
+
+SMALL = [  # (m, k, n, bits, group)
+    (1, 256, 128, 4, 128), (5, 512, 256, 4, 32), (16, 256, 192, 4, 64), (32, 512, 128, 4, 256),
+    (1, 512, 256, 3, 128), (7, 256, 128, 3, 32), (32, 384, 320, 3, 64),
+    (1, 256, 128, 2, 128), (12, 512, 64, 2, 256), (3, 128, 64, 2, 32),
+    (1, 64, 16, 4, 32), (2, 48 * 8, 80, 4, 128), (33, 256, 128, 4, 128), (70, 256, 192, 3, 128),
+]
+
+
+@pytest.mark.parametrize("m,k,n,bits,group", SMALL)
+def test_qgemm_vs_oracle_small(F, orc, gpu, m, k, n, bits, group):
+    rng = np.random.default_rng(1000 + m * 7 + k + n + bits * 3 + group)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, _ = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, err, ratio = _within(y16, y64)
+    assert ok, f"max err {err:.4g} ({ratio:.2f}x bound)"
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 7, 16, 148, 300])
+def test_qgemm_workers_sweep_vs_reference_engine(F, orc, gpu, workers):
+    """Stream-K with P CTAs (incl. P > SM count -> ticketed worker ids) vs the
+    reference engine's own output at the reference layout (y_ref) and y64."""
+    rng = np.random.default_rng(workers)
+    m, k, n, bits, group = 9, 1024, 512, 4, 128
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, _ = _gemm(F, gpu, idx, scales, table, x16, bits, group, workers=workers)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    assert _within(y16, y64)[0]
+    slices = orc.pack(idx, bits)
+    yref, _ = orc.execute(x16, slices, k, n, bits, group, scales, table, workers=min(workers, 8))
+    ok, err, _ = _within(y16, yref.view(np.float16).astype(np.float64))
+    assert ok, err
+
+
+def test_qgemm_deterministic_and_split_free_bitwise(F, orc, gpu):
+    """Bitwise reproducible across runs; P=1 == P=2 when no tile is split
+    (test_engine.cpp:183-206 restated for the device unit grid)."""
+    rng = np.random.default_rng(7)
+    m, k, n, bits, group = 4, 512, 256, 3, 64   # device grid: 4 n-tiles x 4 k-tiles
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    dw = F.DeviceWeights(idx, scales, table, bits, group)
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    outs = [dw.gemm(x, workers=P).cpu().numpy().view(np.uint16) for P in (1, 1, 2, 4)]
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[0], outs[3])
+    splits = [dw.gemm(x, workers=P).cpu().numpy().view(np.uint16) for P in (3, 3)]
+    assert np.array_equal(splits[0], splits[1])
+
+
+def test_host_e2e_equals_device_path(F, orc, gpu):
+    rng = np.random.default_rng(11)
+    m, k, n, bits, group = 3, 1024, 384, 4, 128
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y_dev, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    assert np.array_equal(dw.gemm_host(x16), y_dev)
+
+
+def test_device_layout_upload_path(F, orc, gpu):
+    """flute_weights_create from device-layout buffers == from indices."""
+    rng = np.random.default_rng(12)
+    m, k, n, bits, group = 2, 512, 128, 3, 128
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y_a, _ = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    dw = F.DeviceWeights.from_device_layout(F.pack_device(idx, bits, group),
+                                            F.scales_device(scales, k, n, group),
+                                            F.make_vectorized_lut(table, bits), k, n, bits, group)
+    assert np.array_equal(dw.gemm_host(x16), y_a)
+
+
+def test_raw_qgemm_abi(F, orc, gpu):
+    """flute_qgemm with caller-owned device buffers and workspace."""
+    torch = gpu
+    rng = np.random.default_rng(13)
+    m, k, n, bits, group = 8, 768, 320, 2, 64
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    wdev = torch.from_numpy(F.pack_device(idx, bits, group)).cuda()
+    sdev = torch.from_numpy(F.scales_device(scales, k, n, group).view(np.int16)).cuda()
+    vdev = torch.from_numpy(F.vlut_device_words(F.make_vectorized_lut(table, bits), bits)
+                            .view(np.int32)).cuda()
+    ws = torch.zeros(F.workspace_bytes(m, 148), dtype=torch.uint8, device="cuda")
+    x = torch.from_numpy(x16.view(np.float16)).cuda()
+    y = F.qgemm(x, wdev, sdev, vdev, bits, group, n, ws, workers=0)
+    torch.cuda.synchronize()
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    assert _within(y.cpu().numpy().view(np.uint16), y64)[0]
+    # the workspace is left zeroed (flags re-armed) -> a second call is identical
+    y2 = F.qgemm(x, wdev, sdev, vdev, bits, group, n, ws, workers=0)
+    assert torch.equal(y, y2)
+    P = F.default_workers(m, k, n, bits)
+    assert int(ws[: 4 * (P + 2)].sum()) == 0   # flags + ticket counters back to zero
+
+
+def test_reference_engine_cases(F, orc, gpu):
+    """test_engine.cpp:81-139 restated: constant column, identity activations."""
+    # identity X reproduces dequantized rows to one f16 rounding
+    rng = np.random.default_rng(0xE1)
+    k, n, bits, group = 32, 16, 4, 32
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    idx, scales = F.quantize_matrix(w, bits, group)
+    table = F.build_nf_table(bits)
+    x16 = f16_bits(orc, np.eye(k))
+    y16, _ = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    deq = np.array([[orc.f16_to_f32(
+        orc.vec_dequantize(F.make_vectorized_lut(table, bits)[int(idx[i, j]) << bits],
+                           int(scales[j * (k // group) + i // group])) & 0xFFFF)
+        for j in range(n)] for i in range(k)])
+    assert np.array_equal(y16.view(np.float16).astype(np.float64), deq)
+
+
+@pytest.mark.parametrize("case", ["identity", "zero", "random", "deterministic", "odd_dims"])
+def test_mma_fragment_tensor_core(F, orc, gpu, case):
+    """test_mma.cpp:26-100 restated against the tensor-core mma_fragment."""
+    rng = np.random.default_rng(0xACC)
+    if case == "identity":
+        a = f16_bits(orc, np.eye(4)); b = f16_bits(orc, rng.uniform(-4, 4, (4, 3)))
+        c = F.mma_fragment(a, b, np.zeros((4, 3)))
+        assert np.array_equal(c, b.view(np.float16).astype(np.float32))
+    elif case == "zero":
+        a = np.zeros((2, 2), np.uint16); b = f16_bits(orc, rng.uniform(-1, 1, (2, 2)))
+        c0 = np.array([[1.5, -2.25], [0.125, 3.0]], np.float32)
+        assert np.array_equal(F.mma_fragment(a, b, c0), c0)
+    elif case in ("random", "deterministic"):
+        for _ in range(50 if case == "random" else 1):
+            a = f16_bits(orc, rng.uniform(-1, 1, (16, 16))); b = f16_bits(orc, rng.uniform(-1, 1, (16, 8)))
+            c = F.mma_fragment(a, b, np.zeros((16, 8)))
+            af = a.view(np.float16).astype(np.float64); bf = b.view(np.float16).astype(np.float64)
+            ref = af @ bf
+            bound = 16 * 2.0 ** -24 * np.abs(af).max(1)[:, None] * np.abs(bf).max(0)[None, :]
+            assert np.all(np.abs(c - ref) <= bound)
+            if case == "deterministic":
+                assert np.array_equal(c, F.mma_fragment(a, b, np.zeros((16, 8))))
+    else:
+        a = f16_bits(orc, rng.uniform(-1, 1, (5, 7))); b = f16_bits(orc, rng.uniform(-1, 1, (7, 3)))
+        c = F.mma_fragment(a, b, np.ones((5, 3)))
+        ref = 1 + a.view(np.float16).astype(np.float64) @ b.view(np.float16).astype(np.float64)
+        assert np.allclose(c, ref, atol=1e-5)
+
+
+def test_gpu_error_paths(F, orc, gpu):
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, 16, (64, 48)).astype(np.uint8)
+    table = F.build_nf_table(4)
+    with pytest.raises(F.ConfigError):   # n not a multiple of 16
+        F.DeviceWeights(idx[:, :40], np.ones(40 * 2, np.uint16), table, 4, 32)
+    with pytest.raises(F.ConfigError):   # group does not divide k
+        F.DeviceWeights(idx, np.ones(48, np.uint16), table, 4, 128)
+    with pytest.raises(F.InputError):    # index >= 2^bits
+        F.DeviceWeights(idx, np.ones(48 * 2, np.uint16), F.build_nf_table(3), 3, 32)
+    dw = F.DeviceWeights(idx, np.ones(48 * 2, np.uint16), table, 4, 32)
+    with pytest.raises(F.InputError):
+        dw.gemm(gpu.zeros((2, 32), dtype=gpu.float16, device="cuda"))
+
+
+BASE = [  # BASELINE.json configs at full size (parity by the same bound)
+    (1, 4096, 4096, 4, 128), (16, 4096, 4096, 4, 128),
+    (1, 4096, 14336, 3, 128), (32, 4096, 14336, 3, 128), (4, 14336, 4096, 3, 128),
+    (1, 8192, 8192, 2, 256), (8, 8192, 8192, 4, 32),
+]
+
+
+@pytest.mark.parametrize("m,k,n,bits,group", BASE)
+def test_qgemm_baseline_shapes(F, orc, gpu, m, k, n, bits, group):
+    rng = np.random.default_rng(k + n + m + bits)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, err, ratio = _within(y16, y64)
+    assert ok, f"max err {err:.4g} ({ratio:.2f}x bound)"
+    # size-independent property: linearity in X (y(2x) == 2 y(x) exactly in f16 range)
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    y2 = dw.gemm(x * 2).cpu().numpy().astype(np.float64)
+    y1 = y16.view(np.float16).astype(np.float64)
+    normal = np.abs(y1) >= 2.0 ** -14   # f16 subnormal outputs round on a fixed grid
+    assert np.array_equal(y2[normal], 2 * y1[normal])
