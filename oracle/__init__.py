@@ -93,6 +93,8 @@ class Oracle:
                                        C.c_int, C.c_int, C.c_int, _u64p]
         L.orc_reference_f64.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                         _u8p, _u16p, _f32p, _f64p]
+        L.orc_reference_f64_mode.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             _u8p, _u16p, _f32p, C.c_int, _f64p]
 
     @staticmethod
     def _chk(rc: int, what: str) -> None:
@@ -194,15 +196,18 @@ class Oracle:
                                             tile_m, st), "plan_traffic")
         return st
 
-    def reference_f64(self, x16, idx, bits, group, scales, table) -> np.ndarray:
+    def reference_f64(self, x16, idx, bits, group, scales, table, f16_weights=True) -> np.ndarray:
+        """binary64 X * W_hat.  f16_weights=True: W_hat = the f16 weights the
+        kernel multiplies; False: dequantize_matrix's binary32 weights."""
         x16 = np.ascontiguousarray(x16, np.uint16)
         idx = np.ascontiguousarray(idx, np.uint8)
         m, k = x16.shape
         n = idx.shape[1]
         y = np.zeros((m, n), np.float64)
-        self._chk(self.lib.orc_reference_f64(x16, m, k, n, bits, group, idx,
-                                             np.ascontiguousarray(scales, np.uint16),
-                                             np.ascontiguousarray(table, np.float32), y),
+        self._chk(self.lib.orc_reference_f64_mode(x16, m, k, n, bits, group, idx,
+                                                  np.ascontiguousarray(scales, np.uint16),
+                                                  np.ascontiguousarray(table, np.float32),
+                                                  1 if f16_weights else 0, y),
                   "reference_f64")
         return y
 

@@ -512,6 +512,12 @@ int orc_execute(const uint16_t* x, int m, int k, int n, int bits, int group, con
 int orc_reference_f64(const uint16_t* x, int m, int k, int n, int bits, int group,
                       const uint8_t* idx, const uint16_t* scales, const float* table,
                       double* y64) {
+  return orc_reference_f64_mode(x, m, k, n, bits, group, idx, scales, table, 1, y64);
+}
+
+int orc_reference_f64_mode(const uint16_t* x, int m, int k, int n, int bits, int group,
+                           const uint8_t* idx, const uint16_t* scales, const float* table,
+                           int f16_weights, double* y64) {
   (void)bits;
   const int gpc = k / group;
   double* wd = (double*)malloc(sizeof(double) * (size_t)k * n);
@@ -520,7 +526,10 @@ int orc_reference_f64(const uint16_t* x, int m, int k, int n, int bits, int grou
   for (int i = 0; i < k; ++i)
     for (int j = 0; j < n; ++j)
       wd[(size_t)i * n + j] =
-          orc_f16_to_f32(deq(idx[(size_t)i * n + j], scales[(size_t)j * gpc + i / group], table));
+          f16_weights
+              ? orc_f16_to_f32(deq(idx[(size_t)i * n + j], scales[(size_t)j * gpc + i / group], table))
+              /* dequantize_matrix (quantize.cpp:130-139): binary32 s * T, no f16 rounding */
+              : (double)(orc_f16_to_f32(scales[(size_t)j * gpc + i / group]) * table[idx[(size_t)i * n + j]]);
   memset(y64, 0, sizeof(double) * (size_t)m * n);
 #pragma omp parallel for schedule(static)
   for (int j0 = 0; j0 < n; j0 += 64) {
