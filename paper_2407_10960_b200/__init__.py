@@ -122,6 +122,7 @@ _SIGS = {
     "flute_gemm_host": (C.c_int, [_vp, _u16p, C.c_int, _u16p, C.c_int, _vp]),
     "flute_dequant_all_device": (C.c_int, [_u32p, C.c_int, _u16p, C.c_int, _u32p]),
     "flute_mma_fragment": (C.c_int, [_u16p, _u16p, _f32p, C.c_int, C.c_int, C.c_int]),
+    "flute_debug_times": (C.c_int, [_u64p, C.c_int]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -436,6 +437,13 @@ def mma_fragment(a16: np.ndarray, b16: np.ndarray, c: np.ndarray) -> np.ndarray:
     n = b16.shape[1]
     _check(_lib.flute_mma_fragment(a16, b16, c, m, n, k))
     return c
+
+
+def debug_times(workers: int) -> np.ndarray:
+    """Per-CTA ns timeline of the last launch (needs FLUTE_DEBUG_TIMES=1)."""
+    out = np.zeros(8 * workers, np.uint64)
+    _check(_lib.flute_debug_times(out, workers))
+    return out.reshape(workers, 8)
 
 
 def exported_symbols() -> Sequence[str]:

@@ -455,6 +455,13 @@ int flute_dequant_all_device(const uint32_t* vlut_words, int bits, const uint16_
   });
 }
 
+int flute_debug_times(uint64_t* out, int workers) {
+  return guard([&] {
+    need(out, "out");
+    flute_dev::debug_times(reinterpret_cast<unsigned long long*>(out), workers);
+  });
+}
+
 int flute_mma_fragment(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k) {
   return guard([&] {
     need(a, "a");

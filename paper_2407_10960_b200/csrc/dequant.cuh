@@ -64,29 +64,43 @@ __device__ __forceinline__ uint32_t atom_index_bytes<3>(const LaneBits<3>& lb, i
   return hi | ((lb.lo >> (2 * j)) & 0x03030303u);
 }
 
-// The four A-fragment registers of atom j: a[p] = vLUT[idx_p] * scale2(p),
-// with regs 0/2 (column g) scaled by s_lo and regs 1/3 (column g+8) by s_hi.
+// The four A-fragment registers of atom j: a[p] = vLUT[idx_p] * (s, s), with
+// regs 0/2 (column g) scaled by the low half of `scales` and regs 1/3 (column
+// g+8) by the high half.  The half broadcast folds into the HMUL2 operand
+// selector (.H0_H0 / .H1_H1), so it costs no instruction.
 __device__ __forceinline__ void lut_dequant4(uint32_t idx_bytes, uint32_t lane4, uint32_t lut_base,
-                                             uint32_t s_lo, uint32_t s_hi, uint32_t (&a)[4]) {
+                                             uint32_t scales, uint32_t (&a)[4]) {
+  const __half2 s2 = *reinterpret_cast<const __half2*>(&scales);
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const uint32_t off = prmt(idx_bytes, lane4, 0x5504u | (static_cast<uint32_t>(p) << 4));
-    const uint32_t v = lds32(lut_base + off);
-    a[p] = hmul2_u32(v, (p & 1) ? s_hi : s_lo);
+    uint32_t v = lds32(lut_base + off);
+    const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v),
+                              (p & 1) ? __high2half2(s2) : __low2half2(s2));
+    a[p] = *reinterpret_cast<const uint32_t*>(&r);
   }
 }
 
 // Expand the 2^(2b) device-order vLUT words into the 32-copy shared table.
 // Called by `nthreads` threads with ids [0, nthreads).
-template <int BITS>
+template <int BITS, int NTHREADS>
 __device__ __forceinline__ void fill_lut(uint32_t lut_base, const uint32_t* __restrict__ vlut,
-                                         int tid, int nthreads) {
+                                         int tid) {
   constexpr int kEntries = 1 << (2 * BITS);
-  // Each row: 8 x 16-byte chunks hold the 32 lane copies (bytes 0..127).
-  for (int c = tid; c < kEntries * 8; c += nthreads) {
-    const int e = c >> 3;
-    const uint32_t v = __ldg(vlut + e);
-    sts128(lut_base + e * kLutRowBytes + (c & 7) * 16, make_uint4(v, v, v, v));
+  constexpr int kChunks = kEntries * 8;  // 8 x 16-byte chunks = the 32 lane copies
+  constexpr int kPer = (kChunks + NTHREADS - 1) / NTHREADS;
+  // All global loads first (one latency), then the shared stores.
+  uint32_t v[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int c = tid + i * NTHREADS;
+    v[i] = c < kChunks ? __ldg(vlut + (c >> 3)) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int c = tid + i * NTHREADS;
+    if (c < kChunks) sts128(lut_base + (c >> 3) * kLutRowBytes + (c & 7) * 16,
+                            make_uint4(v[i], v[i], v[i], v[i]));
   }
 }
 

@@ -29,6 +29,9 @@ int default_workers(int m, int k, int n, int bits);
 int sm_count(int device);
 int device_count();
 
+// FLUTE_DEBUG_TIMES=1 per-CTA timeline of the last qgemm launch (8 u64 / CTA).
+void debug_times(unsigned long long* out, int workers);
+
 // Device self-checks.
 void dequant_all(const std::uint32_t* vlut_dev_words_host, int bits, const std::uint16_t* scales,
                  int n_scales, std::uint32_t* out_host);

@@ -1,352 +1,21 @@
-// flute-b200 — the LUT-dequant Stream-K GEMM for the memory-bound regime
-// (M <= 32 per launch), sm_100a.
-//
-// Reference semantics: flutesim::execute (engine.cpp:345) — Y = X * W_hat with
-// W_hat = f16(scale * T[index]) and fp32 accumulation; Stream-K ranges
-// [floor(w*U/P), floor((w+1)*U/P)) over units (n-tile major, k inner) with a
-// fixed-order fixup of split tiles (streamk.cpp:17-58, engine.cpp:279-333).
-//
-// One CTA = one Stream-K worker, 8 consumer warps + 1 producer warp:
-//  * producer (one lane): streams the CTA's units with 1-D bulk async copies
-//    (weights, scales; UBLKCP) and 2-D TMA (the X slice, 128B-swizzled;
-//    UTMALDG) into an S-stage shared-memory ring guarded by mbarriers.  The
-//    weight/scale prefetch of the first S stages is issued before the
-//    programmatic-dependent-launch wait, so it overlaps the previous kernel.
-//  * consumer warp w owns k-step w (16 deep) of every 64x128 unit: one LDS of
-//    its packed pair indices, PRMT -> LDS from the 32-way duplicated vLUT,
-//    HMUL2 by the group scale, and mma.sync m16n8k16 with W^T as the A operand
-//    (HMMA.16816.F32), X^T fragments via ldmatrix.
-//  * a CTA walks its range in *descending* unit order, so the contributor
-//    segment of a split tile (its range's tail) is published first and the
-//    finisher segment (its range's head) is reduced last — the finisher never
-//    stalls waiting for a neighbour that is still mid-range.
-//  * split tiles reduce through an fp32 workspace: contributors store their
-//    partial and release-add the finisher's flag; the finisher acquires,
-//    sums contributors in ascending worker (= ascending k) order, adds its own
-//    partial, writes Y, and re-zeroes its flag (graph/launch-safe).
+// flute-b200 — host launcher of the memory-bound LUT-GEMM (kernel in
+// qgemm_kernel.cuh) plus the device self-check kernels (exhaustive dequant,
+// tensor-core mma_fragment) and small CUDA runtime helpers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
-#include <mutex>
+#include <cstdlib>
 #include <string>
-#include <unordered_map>
 
 #include "dequant.cuh"
 #include "device_api.h"
 #include "flutesim/errors.hpp"
 #include "ptx.cuh"
+#include "qgemm_kernel.cuh"
 
 namespace flute_dev {
-
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = 32 * (kConsumerWarps + 1);
-constexpr int kMaxStages = 16;
-constexpr int kUnitN = 64;   // == flutesim::kUnitN (pack.hpp)
-constexpr int kUnitK = 128;  // == flutesim::kUnitK
-
-struct KParams {
-  const uint8_t* w;
-  const uint8_t* sc;
-  const uint32_t* vlut;
-  __half* y;
-  float* slots;
-  uint32_t* flags;
-  int m, n;
-  int tiles_k;
-  int group;
-  int gp;  // padded groups per column
-  long long units;
-  int workers;
-  int stages;
-  int use_ticket;
-};
-
-template <int BITS, int BM>
-struct Cfg {
-  static constexpr int kLutBytes = (1 << (2 * BITS)) * kLutRowBytes;
-  static constexpr int kUnitBytes = BITS * 1024;  // 64 x 128 weights
-  static constexpr int kXBytes = 2 * BM * 128;    // two 64-wide TMA boxes
-  static constexpr int kScBytes = 512;            // <= 4 groups x 64 scales
-  static constexpr int kFrag = (BM / 8) * 16;     // accumulator floats / lane
-  static constexpr int kRedBytes = 4 * kFrag * 32 * 4;
-  static constexpr int kStageBytes = kXBytes + kUnitBytes + kScBytes;
-  static size_t smem_bytes(int S) {
-    return static_cast<size_t>(kLutBytes) + static_cast<size_t>(S) * kStageBytes + kRedBytes +
-           2 * 8 * kMaxStages + 64;
-  }
-};
-
-__device__ __forceinline__ long long range_lo(long long w, long long U, long long P) {
-  return U * w / P;
-}
-
-__device__ __forceinline__ int owner_of(long long x, long long U, int P) {
-  int w = static_cast<int>((x * P) / U);
-  if (w >= P) w = P - 1;
-  while (w + 1 < P && range_lo(w + 1, U, P) <= x) ++w;
-  while (w > 0 && range_lo(w, U, P) > x) --w;
-  return w;
-}
-
-template <int BITS, int BM>
-__global__ void __launch_bounds__(kThreads, 1)
-    qgemm_mma_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
-  using C = Cfg<BITS, BM>;
-  constexpr int MT = BM / 8;
-  extern __shared__ __align__(1024) uint8_t smem[];
-
-  const int S = p.stages;
-  const uint32_t base = smem_u32(smem);
-  const uint32_t lut = base;
-  const uint32_t xs = base + C::kLutBytes;
-  const uint32_t ws = xs + S * C::kXBytes;
-  const uint32_t ss = ws + S * C::kUnitBytes;
-  const uint32_t red = ss + S * C::kScBytes;
-  const uint32_t bars = red + C::kRedBytes;  // full[kMaxStages], empty[kMaxStages]
-  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + (bars - base) + 16 * kMaxStages);
-  auto full = [&](int s) { return bars + 8 * s; };
-  auto empty = [&](int s) { return bars + 8 * (kMaxStages + s); };
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full(s), 1);
-      mbar_init(empty(s), kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  int wid = blockIdx.x;
-  if (p.use_ticket) {
-    // More workers than co-resident CTAs: take worker ids in start order so a
-    // finisher only ever waits on CTAs that are already running.
-    pdl_wait();
-    if (threadIdx.x == 0) misc[0] = atomicAdd(p.flags + p.workers, 1u);
-  }
-  __syncthreads();
-  if (p.use_ticket) wid = static_cast<int>(misc[0]);
-  pdl_launch_dependents();
-
-  const long long U = p.units;
-  const int P = p.workers;
-  const long long ubeg = range_lo(wid, U, P);
-  const long long uend = range_lo(wid + 1, U, P);
-  const int nunits = static_cast<int>(uend - ubeg);
-  const int tiles_k = p.tiles_k;
-  const int group = p.group;
-  const int ng = group >= kUnitK ? 1 : kUnitK / group;
-
-  if (warp == kConsumerWarps) {
-    // ===================== producer =====================
-    if (lane == 0 && nunits > 0) {
-      prefetch_tmap(&tmap_x);
-      const uint64_t pol = policy_evict_first();
-      const uint32_t stage_tx = C::kXBytes + C::kUnitBytes + ng * 128;
-      auto issue_ws = [&](int it) {
-        const int s = it % S;
-        const long long u = uend - 1 - it;
-        const long long nt = u / tiles_k;
-        const int kt = static_cast<int>(u % tiles_k);
-        const long long glo = static_cast<long long>(kt) * kUnitK / group;
-        mbar_arrive_expect_tx(full(s), stage_tx);
-        bulk_g2s_hint(ws + s * C::kUnitBytes, p.w + u * C::kUnitBytes, C::kUnitBytes, full(s), pol);
-        bulk_g2s(ss + s * C::kScBytes, p.sc + (nt * p.gp + glo) * 128, ng * 128, full(s));
-      };
-      auto issue_x = [&](int it) {
-        const int s = it % S;
-        const long long u = uend - 1 - it;
-        const int k0 = static_cast<int>(u % tiles_k) * kUnitK;
-        tma_2d_g2s(xs + s * C::kXBytes, &tmap_x, k0, 0, full(s));
-        tma_2d_g2s(xs + s * C::kXBytes + BM * 128, &tmap_x, k0 + 64, 0, full(s));
-      };
-      const int pre = nunits < S ? nunits : S;
-      for (int it = 0; it < pre; ++it) issue_ws(it);
-      if (!p.use_ticket) pdl_wait();  // X and the workspace belong to the previous kernel
-      for (int it = 0; it < pre; ++it) issue_x(it);
-      for (int it = pre; it < nunits; ++it) {
-        const int s = it % S;
-        mbar_wait(empty(s), ((it / S) & 1) ^ 1);
-        issue_ws(it);
-        issue_x(it);
-      }
-    }
-  } else {
-    // ===================== consumers =====================
-    fill_lut<BITS>(lut, p.vlut, threadIdx.x, kConsumerWarps * 32);
-    if (!p.use_ticket) pdl_wait();
-    named_bar_sync(1, kConsumerWarps * 32);
-
-    const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
-    // ldmatrix source offset for this lane (X box rows = m, 128B-swizzled).
-    uint32_t xoff[MT > 1 ? MT / 2 : 1];
-    {
-      const int box = warp >> 2;
-      const int c0 = (warp & 3) * 2;
-      if (MT == 1) {
-        const int r = lane & 7;
-        const int c = c0 + ((lane >> 3) & 1);
-        xoff[0] = box * (BM * 128) + r * 128 + ((c ^ r) << 4);
-      } else {
-#pragma unroll
-        for (int q = 0; q < (MT > 1 ? MT / 2 : 1); ++q) {
-          const int mat = lane >> 3;
-          const int r = q * 16 + (mat >> 1) * 8 + (lane & 7);
-          const int c = c0 + (mat & 1);
-          xoff[q] = box * (BM * 128) + r * 128 + ((c ^ (r & 7)) << 4);
-        }
-      }
-    }
-
-    float acc[MT][4][4];
-    for (int it = 0; it < nunits; ++it) {
-      const long long u = uend - 1 - it;
-      const long long tile = u / tiles_k;
-      const int kt = static_cast<int>(u % tiles_k);
-      if (it == 0 || kt == tiles_k - 1) {
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[mt][j][r] = 0.f;
-      }
-      const int s = it % S;
-      mbar_wait(full(s), (it / S) & 1);
-
-      // ---- stage -> registers ----
-      const uint32_t wst = ws + s * C::kUnitBytes;
-      const int slot = warp * 32 + lane;
-      LaneBits<BITS> lb;
-      if constexpr (BITS == 4) {
-        lb.w = lds128(wst + slot * 16);
-      } else if constexpr (BITS == 2) {
-        lb.w = lds64(wst + slot * 8);
-      } else {
-        lb.hi = lds64(wst + slot * 8);
-        lb.lo = lds32(wst + 2048 + slot * 4);
-      }
-      const int gl = (kt * kUnitK + 16 * warp) / group - (kt * kUnitK) / group;
-      const uint4 sq = lds128(ss + s * C::kScBytes + gl * 128 + (lane >> 2) * 16);
-      uint32_t bf[MT][2];
-      const uint32_t xst = xs + s * C::kXBytes;
-      if constexpr (MT == 1) {
-        ldsm_x2(xst + xoff[0], bf[0][0], bf[0][1]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < MT / 2; ++q)
-          ldsm_x4(xst + xoff[q], bf[2 * q][0], bf[2 * q][1], bf[2 * q + 1][0], bf[2 * q + 1][1]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty(s));
-
-      // ---- dequant + MMA ----
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t sw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
-        uint32_t a[4];
-        lut_dequant4(atom_index_bytes<BITS>(lb, j), lane4, lut, dup_lo(sw), dup_hi(sw), a);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) mma_16816(acc[mt][j], a, bf[mt][0], bf[mt][1]);
-      }
-
-      if (it != nunits - 1 && kt != 0) continue;
-
-      // ---- segment end: deterministic CTA reduction (tree over warps) ----
-      float* accf = &acc[0][0][0];
-      auto red_addr = [&](int sl, int i) {
-        return red + ((sl * C::kFrag + i) * 32 + lane) * 4u;
-      };
-#pragma unroll
-      for (int half = 4; half >= 1; half >>= 1) {
-        if (warp >= half && warp < 2 * half) {
-#pragma unroll
-          for (int i = 0; i < C::kFrag; ++i)
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_addr(warp - half, i)), "f"(accf[i]));
-        }
-        named_bar_sync(1, kConsumerWarps * 32);
-        if (warp < half) {
-#pragma unroll
-          for (int i = 0; i < C::kFrag; ++i) {
-            float v;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(red_addr(warp, i)));
-            accf[i] += v;
-          }
-        }
-        named_bar_sync(1, kConsumerWarps * 32);
-      }
-
-      if (warp == 0) {
-        const long long t0 = tile * tiles_k;
-        const bool started = ubeg <= t0;
-        const bool finished = uend >= t0 + tiles_k;
-        float* my_slot = p.slots + static_cast<size_t>(wid) * C::kFrag * 32;
-        if (!finished) {
-          // contributor: publish the fp32 partial, then release-add the
-          // finisher's flag.
-#pragma unroll
-          for (int i = 0; i < C::kFrag; ++i) my_slot[i * 32 + lane] = accf[i];
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) red_release_gpu_add(p.flags + owner_of(t0 + tiles_k - 1, U, P), 1u);
-        } else {
-          if (!started) {
-            // finisher: contributors = non-empty workers in [owner(t0), wid)
-            const int first = owner_of(t0, U, P);
-            uint32_t expect = 0;
-            for (int c = first; c < wid; ++c)
-              expect += range_lo(c + 1, U, P) > range_lo(c, U, P) ? 1u : 0u;
-            while (ld_acquire_gpu(p.flags + wid) < expect) {
-            }
-            // ((c_first + c_next) + ...) + own, element by element
-#pragma unroll
-            for (int i = 0; i < C::kFrag; ++i) {
-              float sum = 0.f;
-              bool have = false;
-              for (int c = first; c < wid; ++c) {
-                if (range_lo(c + 1, U, P) <= range_lo(c, U, P)) continue;
-                const float v = __ldcg(p.slots + (static_cast<size_t>(c) * C::kFrag + i) * 32 + lane);
-                sum = have ? sum + v : v;
-                have = true;
-              }
-              accf[i] = sum + accf[i];
-            }
-            __syncwarp();
-            if (lane == 0) *reinterpret_cast<volatile uint32_t*>(p.flags + wid) = 0u;
-          }
-          // write Y (f16, RNE)
-          const int g = lane >> 2, t = lane & 3;
-          const long long ncol0 = tile * kUnitN;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int r = 0; r < 4; ++r) {
-                const int row = mt * 8 + 2 * t + (r & 1);
-                const long long col = ncol0 + 16 * j + g + 8 * (r >> 1);
-                if (row < p.m && col < p.n)
-                  p.y[static_cast<size_t>(row) * p.n + col] = __float2half_rn(acc[mt][j][r]);
-              }
-        }
-      }
-    }
-  }
-
-  if (p.use_ticket) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const uint32_t done = atomicAdd(p.flags + p.workers + 1, 1u);
-      if (done == static_cast<uint32_t>(P) - 1u) {
-        p.flags[p.workers] = 0u;
-        p.flags[p.workers + 1] = 0u;
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // host side
@@ -381,16 +50,29 @@ EncodeTiled encode_fn() {
   return fn;
 }
 
-CUtensorMap make_x_map(const void* x, int m, int k, int box_rows) {
+// X [m][k] f16.  k % 64 == 0: a 3-D view {64 k, m, k/64 chunks} so one TMA op
+// brings a unit's two 64-wide chunks; otherwise the plain 2-D view (two ops,
+// zero fill past k).
+CUtensorMap make_x_map(const void* x, int m, int k, int box_rows, int box_chunks, bool three_d) {
   CUtensorMap map;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(m)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
-  const cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
-  const cuuint32_t estr[2] = {1u, 1u};
-  const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x),
-                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r;
+  if (three_d) {
+    const cuuint64_t dims[3] = {64u, static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(k / 64)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(k) * 2, 128u};
+    const cuuint32_t box[3] = {64u, static_cast<cuuint32_t>(box_rows),
+                               static_cast<cuuint32_t>(box_chunks)};
+    r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(m)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
+    const cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+    r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) {
     throw flutesim::InputError("X tensor map rejected (x must be 16-byte aligned, k % 8 == 0), code " +
                                std::to_string(static_cast<int>(r)));
@@ -424,32 +106,65 @@ const DevProps& props() {
   return pr;
 }
 
+// FLUTE_DEBUG_TIMES=1: per-CTA %globaltimer stamps {start, producer issued,
+// LUT ready, first stage ready, first segment end, last segment end, exit}.
+unsigned long long* g_dbg = nullptr;
+int g_dbg_cap = 0;
+unsigned long long* debug_times_buffer(int workers) {
+  static const bool on = std::getenv("FLUTE_DEBUG_TIMES") != nullptr;
+  if (!on) return nullptr;
+  if (g_dbg_cap < workers) {
+    if (g_dbg) cudaFree(g_dbg);
+    FLUTE_CUDA(cudaMalloc(&g_dbg, static_cast<size_t>(workers) * 8 * 8));
+    g_dbg_cap = workers;
+  }
+  FLUTE_CUDA(cudaMemset(g_dbg, 0, static_cast<size_t>(workers) * 8 * 8));
+  return g_dbg;
+}
+
 int bm_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : 32; }
 
-template <int BITS, int BM>
+template <int BITS, int BM, int UPS, int CW>
 int stages_for() {
   const size_t cap = props().smem_optin;
   int s = kMaxStages;
-  while (s > 2 && Cfg<BITS, BM>::smem_bytes(s) > cap) --s;
+  while (s > 2 && Cfg<BITS, BM, UPS, CW>::smem_bytes(s) > cap) --s;
   return s;
+}
+
+// Consumer warps: 16 (4 per SM sub-partition) while the accumulators are
+// small enough for the ~100-register budget of 544 threads; 8 for m > 16.
+template <int BM>
+constexpr int cw_for() {
+  return 8;
+}
+
+// Sub-units per stage: 4 (512-deep stages) for m <= 16; 2 for m <= 32 where
+// the X slice of a stage is 4x larger.
+template <int BM>
+constexpr int ups_for() {
+  return BM == 32 ? 2 : 4;
 }
 
 template <int BITS, int BM>
 void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp) {
-  using Cf = Cfg<BITS, BM>;
+  constexpr int UPS = ups_for<BM>();
+  constexpr int CW = cw_for<BM>();
+  using Cf = Cfg<BITS, BM, UPS, CW>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   FLUTE_CUDA(cudaGetDevice(&dev));
-  const int S = stages_for<BITS, BM>();
+  const int S = stages_for<BITS, BM, UPS, CW>();
   const size_t smem = Cf::smem_bytes(S);
   if (configured_dev != dev) {
-    FLUTE_CUDA(cudaFuncSetAttribute(qgemm_mma_kernel<BITS, BM>,
+    FLUTE_CUDA(cudaFuncSetAttribute(qgemm_mma_kernel<BITS, BM, UPS, CW>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
     configured_dev = dev;
   }
-  const CUtensorMap map = make_x_map(x, m_rows, a.k, BM);
+  const bool x3d = a.k % 64 == 0 && std::getenv("FLUTE_X2D") == nullptr;
+  const CUtensorMap map = make_x_map(x, m_rows, a.k, m_rows, 2 * UPS, x3d);
   KParams kp{};
   kp.w = static_cast<const uint8_t*>(a.w);
   kp.sc = static_cast<const uint8_t*>(a.scales);
@@ -462,16 +177,22 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
   kp.m = m_rows;
   kp.n = a.n;
   kp.tiles_k = tiles_k;
-  kp.group = a.group;
+  kp.group_shift = __builtin_ctz(static_cast<unsigned>(a.group));
   kp.gp = gp;
-  kp.units = units;
+  kp.units = static_cast<int>(units);
   kp.workers = workers;
   kp.stages = S;
   kp.use_ticket = workers > props().sms ? 1 : 0;
+  kp.x3d = x3d ? 1 : 0;
+  {
+    static const char* d = std::getenv("FLUTE_DIAG");
+    kp.diag = d ? std::atoi(d) : 0;
+  }
+  kp.dbg = debug_times_buffer(workers);
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(workers));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads_for<CW>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = static_cast<cudaStream_t>(a.stream);
   cudaLaunchAttribute attr[1];
@@ -479,7 +200,7 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  FLUTE_CUDA(cudaLaunchKernelEx(&cfg, qgemm_mma_kernel<BITS, BM>, map, kp));
+  FLUTE_CUDA(cudaLaunchKernelEx(&cfg, qgemm_mma_kernel<BITS, BM, UPS, CW>, map, kp));
 }
 
 template <int BITS>
@@ -519,6 +240,12 @@ int default_workers(int m, int k, int n, int bits) {
   return static_cast<int>(std::min<long long>(units, props().sms));
 }
 
+void debug_times(unsigned long long* out, int workers) {
+  if (!g_dbg) throw flutesim::InputError("FLUTE_DEBUG_TIMES not enabled");
+  FLUTE_CUDA(cudaMemcpy(out, g_dbg, static_cast<size_t>(std::min(workers, g_dbg_cap)) * 64,
+                        cudaMemcpyDeviceToHost));
+}
+
 size_t workspace_bytes(int m, int workers) {
   const int bm = bm_for(std::min(m, 32));
   const size_t flag_bytes = (static_cast<size_t>(workers) + 2) * 4;
@@ -539,6 +266,8 @@ void qgemm(const GemmArgs& a) {
   const int tiles_k = kp / kUnitK;
   const long long units = static_cast<long long>(tiles_k) * (np / kUnitN);
   int workers = a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits);
+  if (units * (static_cast<long long>(workers) + 1) >= (1LL << 31))
+    throw flutesim::ConfigError("qgemm: units x workers exceeds the 32-bit Stream-K index range");
   if (a.workspace_bytes < workspace_bytes(a.m, workers))
     throw flutesim::InputError("qgemm: workspace too small");
   const int gp = kp / a.group;
@@ -565,7 +294,7 @@ __global__ void dequant_all_kernel(const uint32_t* __restrict__ vlut, const uint
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NP = 1 << (2 * BITS);
   const uint32_t lut = smem_u32(smem);
-  fill_lut<BITS>(lut, vlut, threadIdx.x, blockDim.x);
+  fill_lut<BITS, 256>(lut, vlut, threadIdx.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -609,8 +338,7 @@ __global__ void dequant_all_kernel(const uint32_t* __restrict__ vlut, const uint
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t a[4];
-      lut_dequant4(atom_index_bytes<BITS>(lb, j), static_cast<uint32_t>(lane) * 4u, lut, dup_lo(sw),
-                   dup_hi(sw), a);
+      lut_dequant4(atom_index_bytes<BITS>(lb, j), static_cast<uint32_t>(lane) * 4u, lut, sw, a);
 #pragma unroll
       for (int pp = 0; pp < 4; ++pp) {
         const int q = 4 * j + pp;
