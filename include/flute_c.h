@@ -130,10 +130,12 @@ int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y
  * reference order (the routine applies the device index permutation). */
 int flute_dequant_all_device(const uint32_t* vlut_words, int bits, const uint16_t* scales,
                              int n_scales, uint32_t* out_host);
-/* Diagnostics: with FLUTE_DEBUG_TIMES=1 in the environment, each qgemm
- * launch records per-CTA %globaltimer stamps (ns) {start, producer issued,
- * LUT ready, first stage landed, segment end, last segment end, exit, -};
- * copies 8*workers values of the last launch. */
+/* Diagnostics (libflute_b200_diag.so only; `make diag`): with
+ * FLUTE_DEBUG_TIMES=1, each qgemm launch records per-CTA %globaltimer stamps
+ * (ns) {start, producer issued, LUT ready, first stage landed, segment end,
+ * last segment end, exit, finisher acquired} (8*workers values) followed by a
+ * per-stage trace of consumer warp 0 (workers*64*3 values: wait begin, data
+ * ready, compute done); copies all 200*workers values of the last launch. */
 int flute_debug_times(uint64_t* out, int workers);
 /* mma_fragment on the tensor cores (mma.hpp:23); host buffers. */
 int flute_mma_fragment(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);

@@ -21,7 +21,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflute_b200.so")
+LIB_PATH = os.environ.get("FLUTE_LIB") or os.path.join(_HERE, "libflute_b200.so")
 
 DEFAULT_LAYOUT = (16, 64, 64, 16, 8, 16)  # reference pack.hpp:21-26
 UNIT_N, UNIT_K = 64, 128                  # device Stream-K unit (pack.hpp kUnitN/kUnitK)
@@ -441,9 +441,9 @@ def mma_fragment(a16: np.ndarray, b16: np.ndarray, c: np.ndarray) -> np.ndarray:
 
 def debug_times(workers: int) -> np.ndarray:
     """Per-CTA ns timeline of the last launch (needs FLUTE_DEBUG_TIMES=1)."""
-    out = np.zeros(8 * workers, np.uint64)
+    out = np.zeros(200 * workers, np.uint64)
     _check(_lib.flute_debug_times(out, workers))
-    return out.reshape(workers, 8)
+    return out[:8 * workers].reshape(workers, 8), out[8 * workers:].reshape(workers, 64, 3)
 
 
 def exported_symbols() -> Sequence[str]:

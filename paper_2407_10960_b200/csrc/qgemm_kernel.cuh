@@ -7,26 +7,29 @@
 // (n-tile major, k inner; streamk.cpp:17-58) with a fixed-order fixup of split
 // tiles (engine.cpp:279-333).
 //
-// One CTA = one Stream-K worker: 8 consumer warps + 1 producer warp.
-//  * Stages.  The CTA walks its sub-units in descending order and groups up
-//    to UPS consecutive sub-units of the same 64-column tile into one stage:
-//    its weights and scales are contiguous in the device layout (one 1-D bulk
-//    copy each, UBLKCP) and its X slice is one 3-D TMA box {64 k, BM rows,
-//    2*UPS chunks}, 128B-swizzled (UTMALDG).  Three copies per stage keep the
-//    single producer thread far ahead of HBM.  The weight/scale copies of the
-//    first S stages are issued before the programmatic-dependent-launch wait,
-//    so they overlap the previous kernel in the stream.
-//  * Consumer warp w owns k-steps {w, w+8, ...} of a stage: LDS of its packed
-//    pair indices, PRMT -> LDS from the 32-way duplicated vLUT, HMUL2 by the
-//    group scale (operand-selector broadcast), mma.sync m16n8k16 with W^T as
-//    the A operand (HMMA.16816.F32), X^T fragments via ldmatrix.
-//  * Descending walk: a split tile's contributor segment (the range's tail) is
-//    processed first and published early; the finisher segment (the range's
-//    head) is reduced last, so the finisher rarely waits.
-//  * Split tiles reduce through an fp32 workspace: contributors store their
-//    partial and release-add the finisher's flag; the finisher acquires, sums
-//    contributors in ascending worker (= ascending k) order, adds its own
-//    partial, writes Y and re-arms its flag (graph / back-to-back safe).
+// One CTA = one Stream-K worker = 8 consumer warps + 1 producer warp + 1
+// epilogue warp, all synchronised through mbarriers only (no CTA barrier in
+// the steady state):
+//  * Producer.  Walks the CTA's sub-units in descending order, grouping up to
+//    UPS consecutive sub-units of one 64-column tile into a stage: weights and
+//    scales are contiguous in the device layout (one 1-D bulk copy each,
+//    UBLKCP) and the X slice is one 3-D TMA box {64 k, m rows, 2*UPS chunks},
+//    128B-swizzled (UTMALDG).  The weight/scale copies of the first S stages
+//    are issued before the programmatic-dependent-launch wait, so they overlap
+//    the previous kernel in the stream.
+//  * Consumer warp w owns k-step w of every sub-unit: LDS of its packed pair
+//    indices, PRMT -> LDS from the 32-way duplicated vLUT, HMUL2 by the group
+//    scale (operand-selector broadcast), mma.sync m16n8k16 with W^T as the A
+//    operand (HMMA.16816.F32), X^T fragments via ldmatrix.  At the end of an
+//    output-tile segment it parks its fp32 partial in shared memory, arrives
+//    on `epi_full` and goes straight on with the next stage.
+//  * Epilogue warp.  Sums the 8 warp partials in fixed order (deterministic),
+//    releases the buffer (`epi_empty`), then does the Stream-K fixup off the
+//    critical path: contributors publish their fp32 partial and release-add
+//    the finisher's flag; finishers acquire, add contributors in ascending
+//    worker (= ascending k) order, add their own partial, write Y and re-arm
+//    their flag (graph / back-to-back safe).  The descending walk processes a
+//    split tile's contributor segment first, so finishers rarely wait.
 #pragma once
 
 #include <cuda.h>
@@ -39,11 +42,10 @@
 
 namespace flute_dev {
 
-// Consumer warps per CTA: CW in {8, 16} (template); plus one producer warp.
-template <int CW>
-constexpr int threads_for() {
-  return 32 * (CW + 1);
-}
+constexpr int kConsumerWarps = 8;
+constexpr int kProducerWarp = kConsumerWarps;
+constexpr int kEpilogueWarp = kConsumerWarps + 1;
+constexpr int kThreads = 32 * (kConsumerWarps + 2);
 constexpr int kMaxStages = 16;
 constexpr int kUnitN = 64;   // == flutesim::kUnitN (pack.hpp)
 constexpr int kUnitK = 128;  // == flutesim::kUnitK: one Stream-K sub-unit
@@ -64,25 +66,24 @@ struct KParams {
   int stages;
   int use_ticket;
   int x3d;   // X tensor map is the 3-D {64, m, k/64} view (k % 64 == 0)
-  int diag;  // FLUTE_DIAG bits (diagnostics; results are wrong when set):
+  int diag;  // FLUTE_DIAG bits (diag build only; results are wrong when set):
              // 1 skip dequant/MMA, 2 skip weight loads, 4 skip X, 8 skip scales
-  unsigned long long* dbg;  // optional per-CTA timeline (FLUTE_DEBUG_TIMES)
+  unsigned long long* dbg;  // per-CTA timeline (diag build, FLUTE_DEBUG_TIMES)
 };
 
-template <int BITS, int BM, int UPS, int CW>
+template <int BITS, int BM, int UPS>
 struct Cfg {
   static constexpr int kLutBytes = (1 << (2 * BITS)) * kLutRowBytes;
-  static constexpr int kSubBytes = BITS * 1024;             // 64 x 128 weights
-  static constexpr int kChunks = 2 * UPS;                   // 64-wide k chunks of X
-  static constexpr int kXBytes = kChunks * BM * 128;
+  static constexpr int kSubBytes = BITS * 1024;  // 64 x 128 weights
+  static constexpr int kXBytes = 2 * UPS * BM * 128;
   static constexpr int kWBytes = UPS * kSubBytes;
-  static constexpr int kScBytes = UPS * 4 * 128;            // <= 4 groups per sub-unit
-  static constexpr int kFrag = (BM / 8) * 16;               // accumulator floats / lane
-  static constexpr int kRedBytes = (CW / 2) * kFrag * 32 * 4 + 128;  // + a zero row for ldmatrix
+  static constexpr int kScBytes = UPS * 4 * 128;  // <= 4 groups per sub-unit
+  static constexpr int kFrag = (BM / 8) * 16;     // accumulator floats / lane
+  static constexpr int kPartBytes = kConsumerWarps * kFrag * 32 * 4;
   static constexpr int kStageBytes = kXBytes + kWBytes + kScBytes;
   static constexpr size_t smem_bytes(int S) {
-    return static_cast<size_t>(kLutBytes) + static_cast<size_t>(S) * kStageBytes + kRedBytes +
-           2 * 8 * kMaxStages + 64;
+    return static_cast<size_t>(kLutBytes) + static_cast<size_t>(S) * kStageBytes + kPartBytes +
+           8 * (2 * kMaxStages + 2) + 64;
   }
 };
 
@@ -91,10 +92,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Diagnostics (timeline stamps, FLUTE_DIAG bits) exist only in builds with
+// -DFLUTE_DIAGNOSTICS (make diag); the product build compiles them out.
+#ifdef FLUTE_DIAGNOSTICS
 #define FLUTE_STAMP(slot)                                                     \
   do {                                                                        \
     if (p.dbg) p.dbg[static_cast<size_t>(blockIdx.x) * 8 + (slot)] = gtimer(); \
   } while (0)
+#define FLUTE_DIAG(bit) ((p.diag & (bit)) != 0)
+#else
+#define FLUTE_STAMP(slot) \
+  do {                    \
+  } while (0)
+#define FLUTE_DIAG(bit) false
+#endif
 
 // Host guarantees units * (workers + 1) < 2^31, so 32-bit math is exact.
 __device__ __forceinline__ int range_lo(int w, int U, int P) {
@@ -112,7 +123,8 @@ __device__ __forceinline__ int owner_of(int x, int U, int P) {
 }
 
 // Descending walk over a CTA range in stages of <= UPS sub-units that never
-// cross a tile boundary.  Producer and consumers run identical copies.
+// cross a tile boundary.  Producer, consumers and the epilogue warp run
+// identical copies.
 template <int UPS>
 struct StageWalk {
   int hi, tile, kt;  // highest remaining sub-unit, its tile and k-slice
@@ -127,6 +139,9 @@ struct StageWalk {
     nsub = hi - ubeg + 1 < n ? hi - ubeg + 1 : n;
     lo_kt = kt - nsub + 1;
   }
+  __device__ __forceinline__ bool seg_end(int ubeg) const {
+    return lo_kt == 0 || hi - nsub + 1 == ubeg;
+  }
   __device__ __forceinline__ void next(int tiles_k) {
     hi -= nsub;
     if (lo_kt == 0) {
@@ -138,12 +153,10 @@ struct StageWalk {
   }
 };
 
-template <int BITS, int BM, int UPS, int CW>
-__global__ void __launch_bounds__(threads_for<CW>(), 1)
+template <int BITS, int BM, int UPS>
+__global__ void __launch_bounds__(kThreads, 1)
     qgemm_mma_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
-  using C = Cfg<BITS, BM, UPS, CW>;
-  constexpr int kConsumerWarps = CW;
-  constexpr int R = CW / 8;  // warps sharing one k-step: warp w takes sub-units r == w/8 (mod R)
+  using C = Cfg<BITS, BM, UPS>;
   constexpr int MT = BM / 8;
   extern __shared__ __align__(1024) uint8_t smem[];
 
@@ -153,11 +166,13 @@ __global__ void __launch_bounds__(threads_for<CW>(), 1)
   const uint32_t xs = base + C::kLutBytes;
   const uint32_t ws = xs + S * C::kXBytes;
   const uint32_t ss = ws + S * C::kWBytes;
-  const uint32_t red = ss + S * C::kScBytes;
-  const uint32_t bars = red + C::kRedBytes;  // full[kMaxStages], empty[kMaxStages]
-  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + (bars - base) + 16 * kMaxStages);
+  const uint32_t part = ss + S * C::kScBytes;  // [warp][frag][lane] fp32 partials
+  const uint32_t bars = part + C::kPartBytes;
   auto full = [&](int s) { return bars + 8 * s; };
   auto empty = [&](int s) { return bars + 8 * (kMaxStages + s); };
+  const uint32_t epi_full = bars + 8 * (2 * kMaxStages);
+  const uint32_t epi_empty = epi_full + 8;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + (epi_empty + 8 - base));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -166,8 +181,10 @@ __global__ void __launch_bounds__(threads_for<CW>(), 1)
     FLUTE_STAMP(0);
     for (int s = 0; s < S; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), kConsumerWarps);
+      mbar_init(empty(s), kConsumerWarps * 32);  // every consumer thread arrives
     }
+    mbar_init(epi_full, kConsumerWarps * 32);
+    mbar_init(epi_empty, 32);
     fence_mbar_init();
   }
   int wid = blockIdx.x;
@@ -188,29 +205,34 @@ __global__ void __launch_bounds__(threads_for<CW>(), 1)
   const int tiles_k = p.tiles_k;
   const int gshift = p.group_shift;
 
-  if (warp == kConsumerWarps) {
+  if (warp == kProducerWarp) {
     // ===================== producer =====================
-    if (lane == 0 && uend > ubeg) {
-      prefetch_tmap(&tmap_x);
+    // The whole warp walks the stages (uniform control flow keeps addresses in
+    // uniform registers); one elected lane issues each copy.
+    if (uend > ubeg) {
+      const bool leader = elect_one();
+      if (leader) prefetch_tmap(&tmap_x);
       const uint64_t pol = policy_evict_first();
-      const bool do_w = !(p.diag & 2), do_x = !(p.diag & 4), do_s = !(p.diag & 8);
+      const bool do_w = !FLUTE_DIAG(2), do_x = !FLUTE_DIAG(4), do_s = !FLUTE_DIAG(8);
       auto issue_ws = [&](const StageWalk<UPS>& sw, int s) {
         const int glo = (sw.lo_kt * kUnitK) >> gshift;
         const int ng = (((sw.kt + 1) * kUnitK - 1) >> gshift) - glo + 1;
         const uint32_t xb = do_x ? (p.x3d ? 2 * UPS : 2 * sw.nsub) * p.m * 128 : 0;
         const uint32_t wb = do_w ? sw.nsub * C::kSubBytes : 0;
         const uint32_t sb = do_s ? ng * 128 : 0;
-        mbar_arrive_expect_tx(full(s), xb + wb + sb);
-        if (wb)
-          bulk_g2s_hint(ws + s * C::kWBytes,
-                        p.w + static_cast<size_t>(sw.hi - sw.nsub + 1) * C::kSubBytes, wb, full(s),
-                        pol);
-        if (sb)
-          bulk_g2s(ss + s * C::kScBytes, p.sc + (static_cast<size_t>(sw.tile) * p.gp + glo) * 128,
-                   sb, full(s));
+        if (leader) {
+          mbar_arrive_expect_tx(full(s), xb + wb + sb);
+          if (wb)
+            bulk_g2s_hint(ws + s * C::kWBytes,
+                          p.w + static_cast<size_t>(sw.hi - sw.nsub + 1) * C::kSubBytes, wb,
+                          full(s), pol);
+          if (sb)
+            bulk_g2s(ss + s * C::kScBytes,
+                     p.sc + (static_cast<size_t>(sw.tile) * p.gp + glo) * 128, sb, full(s));
+        }
       };
       auto issue_x = [&](const StageWalk<UPS>& sw, int s) {
-        if (!do_x) return;
+        if (!do_x || !leader) return;
         if (p.x3d) {
           tma_3d_g2s(xs + s * C::kXBytes, &tmap_x, 0, 0, sw.lo_kt * 2, full(s));
         } else {
@@ -249,50 +271,142 @@ __global__ void __launch_bounds__(threads_for<CW>(), 1)
         }
       }
     }
+  } else if (warp == kEpilogueWarp) {
+    // ===================== epilogue =====================
+    if (!p.use_ticket) pdl_wait();  // the workspace and Y belong to the previous kernel
+    StageWalk<UPS> sw;
+    sw.init(uend, tiles_k);
+    int seg = 0;
+    for (; sw.hi >= ubeg; sw.next(tiles_k)) {
+      sw.shape(ubeg);
+      if (!sw.seg_end(ubeg)) continue;
+      // fixed-order sum of the 8 warp partials, then free the buffer
+      mbar_wait(epi_full, seg & 1);
+      float accf[C::kFrag];
+#pragma unroll
+      for (int i = 0; i < C::kFrag; ++i) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(part + (i * 32 + lane) * 4u));
+        accf[i] = v;
+      }
+#pragma unroll
+      for (int w = 1; w < kConsumerWarps; ++w) {
+#pragma unroll
+        for (int i = 0; i < C::kFrag; ++i) {
+          float v;
+          asm volatile("ld.shared.f32 %0, [%1];"
+                       : "=f"(v)
+                       : "r"(part + ((w * C::kFrag + i) * 32 + lane) * 4u));
+          accf[i] += v;
+        }
+      }
+      mbar_arrive(epi_empty);
+      ++seg;
+
+      const int tile = sw.tile;
+      if (lane == 0) FLUTE_STAMP(sw.hi - sw.nsub + 1 == ubeg ? 5 : 4);
+      const int t0 = tile * tiles_k;
+      const bool started = ubeg <= t0;
+      const bool finished = uend >= t0 + tiles_k;
+      if (!finished) {
+        // contributor: publish the fp32 partial, then release-add the
+        // finisher's flag.
+        float* my_slot = p.slots + static_cast<size_t>(wid) * C::kFrag * 32;
+#pragma unroll
+        for (int i = 0; i < C::kFrag; ++i) my_slot[i * 32 + lane] = accf[i];
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) red_release_gpu_add(p.flags + owner_of(t0 + tiles_k - 1, U, P), 1u);
+        continue;
+      }
+      if (!started) {
+        // finisher: contributors = non-empty workers in [owner(t0), wid)
+        const int first = owner_of(t0, U, P);
+        uint32_t expect = 0;
+        for (int c = first; c < wid; ++c)
+          expect += range_lo(c + 1, U, P) > range_lo(c, U, P) ? 1u : 0u;
+        while (ld_acquire_gpu(p.flags + wid) < expect) {
+        }
+        if (lane == 0) FLUTE_STAMP(7);
+        // ((c_first + c_next) + ...) + own
+        float sum[C::kFrag];
+        bool have = false;
+        for (int c = first; c < wid; ++c) {
+          if (range_lo(c + 1, U, P) <= range_lo(c, U, P)) continue;
+          const float* src = p.slots + static_cast<size_t>(c) * C::kFrag * 32 + lane;
+          if (!have) {
+#pragma unroll
+            for (int i = 0; i < C::kFrag; ++i) sum[i] = __ldcg(src + i * 32);
+          } else {
+#pragma unroll
+            for (int i = 0; i < C::kFrag; ++i) sum[i] += __ldcg(src + i * 32);
+          }
+          have = true;
+        }
+#pragma unroll
+        for (int i = 0; i < C::kFrag; ++i) accf[i] = sum[i] + accf[i];
+        __syncwarp();
+        if (lane == 0) *reinterpret_cast<volatile uint32_t*>(p.flags + wid) = 0u;
+      }
+      // write Y (f16, RNE); accf[(mt*4 + j)*4 + r] is C[n][m] of atom j, m-tile mt
+      const int g = lane >> 2, t = lane & 3;
+      const int ncol0 = tile * kUnitN;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = mt * 8 + 2 * t + (r & 1);
+            const int col = ncol0 + 16 * j + g + 8 * (r >> 1);
+            if (row < p.m && col < p.n)
+              p.y[static_cast<size_t>(row) * p.n + col] = __float2half_rn(accf[(mt * 4 + j) * 4 + r]);
+          }
+    }
   } else {
     // ===================== consumers =====================
     fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
-    if (!p.use_ticket) pdl_wait();
-    named_bar_sync(1, kConsumerWarps * 32);
-    if (threadIdx.x == 0) FLUTE_STAMP(2);
-
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
+    const int kstep = warp;  // 16-deep k step within a sub-unit
     // X stage = TMA box {64 k, m rows, 2*UPS chunks}, compact ([chunk][m][128 B],
     // 128B-swizzled by box row R = chunk*m + row).  ldmatrix lanes whose row is
-    // >= m read a shared zero row instead, so no zero-fill bytes move.
-    const int mrows = p.m;
-    int lrow[MT > 1 ? MT / 2 : 1];  // this lane's ldmatrix row per x4 (or x2)
-    int lcol[MT > 1 ? MT / 2 : 1];  // its 16-byte column chunk within 128 B
+    // >= m read the stage buffer's last 128 bytes, which TMA never writes when
+    // m < BM and which are zeroed here — so no zero-fill bytes move.
+    constexpr int XQ = MT > 1 ? MT / 2 : 1;
+    uint32_t xoff[UPS][XQ];  // per sub-unit r, per ldmatrix: byte offset in a stage
     {
-      const int c0 = ((warp & 7) & 3) * 2;
-      if constexpr (MT == 1) {
-        lrow[0] = lane & 7;
-        lcol[0] = c0 + ((lane >> 3) & 1);
-      } else {
+      const int mrows = p.m;
 #pragma unroll
-        for (int q = 0; q < MT / 2; ++q) {
-          const int mat = lane >> 3;
-          lrow[q] = q * 16 + (mat >> 1) * 8 + (lane & 7);
-          lcol[q] = c0 + (mat & 1);
+      for (int q = 0; q < XQ; ++q) {
+        const int mat = lane >> 3;
+        const int row = MT == 1 ? (lane & 7) : q * 16 + (mat >> 1) * 8 + (lane & 7);
+        const int col = (kstep & 3) * 2 + (MT == 1 ? ((lane >> 3) & 1) : (mat & 1));
+#pragma unroll
+        for (int r = 0; r < UPS; ++r) {
+          const int R = (2 * r + (kstep >> 2)) * mrows + row;
+          xoff[r][q] = row < mrows ? static_cast<uint32_t>(R * 128 + ((col ^ (R & 7)) << 4))
+                                   : static_cast<uint32_t>(C::kXBytes - 128);
         }
       }
+      if (mrows < BM) {
+        for (int i = threadIdx.x; i < S * 8; i += kConsumerWarps * 32)
+          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
+                           xs + (i >> 3) * C::kXBytes + C::kXBytes - 128 + (i & 7) * 16),
+                       "r"(0u));
+      }
     }
-    const uint32_t zrow = red + C::kRedBytes - 128;  // never written by the reduction
-    if (warp == 0) asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(zrow + lane * 16 % 128), "r"(0u));
-    named_bar_sync(1, kConsumerWarps * 32);
-    auto x_addr = [&](uint32_t xstage, int chunk, int q) -> uint32_t {
-      const int row = lrow[q];
-      if (row >= mrows) return zrow;
-      const int R = chunk * mrows + row;
-      return xstage + R * 128 + ((lcol[q] ^ (R & 7)) << 4);
-    };
+    named_bar_sync(1, kConsumerWarps * 32);  // LUT + zero rows visible
+    if (threadIdx.x == 0) FLUTE_STAMP(2);
 
     float acc[MT][4][4];
     StageWalk<UPS> sw;
     sw.init(uend, tiles_k);
-    int s = 0;
+    int s = 0, seg = 0;
     uint32_t ph = 0;
     bool first_stage = true;
+#ifdef FLUTE_DIAGNOSTICS
+    int stage_no = 0;
+#endif
     for (; sw.hi >= ubeg; sw.next(tiles_k), s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u) {
       sw.shape(ubeg);
       if (first_stage || sw.kt == tiles_k - 1) {
@@ -303,67 +417,70 @@ __global__ void __launch_bounds__(threads_for<CW>(), 1)
 #pragma unroll
             for (int r = 0; r < 4; ++r) acc[mt][j][r] = 0.f;
       }
+#ifdef FLUTE_DIAGNOSTICS
+      // per-stage trace of consumer warp 0: {wait begin, data ready, compute done}
+      unsigned long long* trace =
+          (p.dbg && threadIdx.x == 0 && stage_no < 60)
+              ? p.dbg + static_cast<size_t>(gridDim.x) * 8 +
+                    (static_cast<size_t>(blockIdx.x) * 64 + stage_no) * 3
+              : nullptr;
+      if (trace) trace[0] = gtimer();
+#endif
       mbar_wait(full(s), ph);
+#ifdef FLUTE_DIAGNOSTICS
       if (first_stage && threadIdx.x == 0) FLUTE_STAMP(3);
+      if (trace) trace[1] = gtimer();
+#endif
       first_stage = false;
 
       // ---- stage -> registers (all loads first), then dequant + MMA ----
       // NS = sub-units in this stage; full stages (the common case) take the
       // NS = UPS instantiation, free of per-sub-unit predicates.
-      const uint32_t wst = ws + s * C::kWBytes;
-      const uint32_t sst = ss + s * C::kScBytes;
+      // this lane's bytes within a sub-unit: W4 16 B at slot*16; W2 8 B at
+      // slot*8; W3 8 B (2-bit plane) at slot*8 + 4 B (1-bit plane) at 2048+slot*4
+      const int slot = kstep * 32 + lane;
+      const uint32_t wst = ws + s * C::kWBytes + slot * (BITS == 4 ? 16 : 8);
+      const uint32_t sst = ss + s * C::kScBytes + (lane >> 2) * 16;
       const uint32_t xst = xs + s * C::kXBytes;
       const int glo = (sw.lo_kt * kUnitK) >> gshift;
-      const int kstep = warp & 7;   // 16-deep k step within a sub-unit
-      const int rsel = warp >> 3;   // this warp's sub-unit phase (0..R-1)
       auto run_stage = [&](auto ns_tag) {
         constexpr int NS = decltype(ns_tag)::value;
-        constexpr int NR = (NS + R - 1) / R;  // sub-units per warp (upper bound)
-        LaneBits<BITS> lb[NR];
-        uint4 sq[NR];
-        uint32_t bf[NR][MT][2];
-        bool live[NR];
+        LaneBits<BITS> lb[NS];
+        uint4 sq[NS];
+        uint32_t bf[NS][MT][2];
 #pragma unroll
-        for (int rr = 0; rr < NR; ++rr) {
-          const int r = rr * R + rsel;
-          live[rr] = (NS % R == 0) || r < NS;
-          if (!live[rr]) continue;
+        for (int r = 0; r < NS; ++r) {
           const uint32_t wr = wst + r * C::kSubBytes;
-          const int lslot = kstep * 32 + lane;
           if constexpr (BITS == 4) {
-            lb[rr].w = lds128(wr + lslot * 16);
+            lb[r].w = lds128(wr);
           } else if constexpr (BITS == 2) {
-            lb[rr].w = lds64(wr + lslot * 8);
+            lb[r].w = lds64(wr);
           } else {
-            lb[rr].hi = lds64(wr + lslot * 8);
-            lb[rr].lo = lds32(wr + 2048 + lslot * 4);
+            lb[r].hi = lds64(wr);
+            lb[r].lo = lds32(wr - slot * 8 + 2048 + slot * 4);
           }
           const int gl = ((((sw.lo_kt + r) << 7) + 16 * kstep) >> gshift) - glo;
-          sq[rr] = lds128(sst + gl * 128 + (lane >> 2) * 16);
-          const int chunk = 2 * r + (kstep >> 2);
+          sq[r] = lds128(sst + gl * 128);
           if constexpr (MT == 1) {
-            ldsm_x2(x_addr(xst, chunk, 0), bf[rr][0][0], bf[rr][0][1]);
+            ldsm_x2(xst + xoff[r][0], bf[r][0][0], bf[r][0][1]);
           } else {
 #pragma unroll
             for (int q = 0; q < MT / 2; ++q)
-              ldsm_x4(x_addr(xst, chunk, q), bf[rr][2 * q][0], bf[rr][2 * q][1],
-                      bf[rr][2 * q + 1][0], bf[rr][2 * q + 1][1]);
+              ldsm_x4(xst + xoff[r][q], bf[r][2 * q][0], bf[r][2 * q][1], bf[r][2 * q + 1][0],
+                      bf[r][2 * q + 1][1]);
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty(s));
-        if (p.diag & 1) return;
+        mbar_arrive(empty(s));  // each thread, after its own smem reads
+        if (FLUTE_DIAG(1)) return;
 #pragma unroll
-        for (int rr = 0; rr < NR; ++rr) {
-          if (!live[rr]) continue;
+        for (int r = 0; r < NS; ++r) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint32_t scw =
-                j == 0 ? sq[rr].x : j == 1 ? sq[rr].y : j == 2 ? sq[rr].z : sq[rr].w;
+            const uint32_t scw = j == 0 ? sq[r].x : j == 1 ? sq[r].y : j == 2 ? sq[r].z : sq[r].w;
             uint32_t a[4];
-            lut_dequant4(atom_index_bytes<BITS>(lb[rr], j), lane4, lut, scw, a);
+            lut_dequant4(atom_index_bytes<BITS>(lb[r], j), lane4, lut, scw, a);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt) mma_16816(acc[mt][j], a, bf[rr][mt][0], bf[rr][mt][1]);
+            for (int mt = 0; mt < MT; ++mt) mma_16816(acc[mt][j], a, bf[r][mt][0], bf[r][mt][1]);
           }
         }
       };
@@ -372,97 +489,40 @@ __global__ void __launch_bounds__(threads_for<CW>(), 1)
       } else if (sw.nsub == 1) {
         run_stage(std::integral_constant<int, 1>{});
       } else if constexpr (UPS > 2) {
-        if (sw.nsub == 2) run_stage(std::integral_constant<int, 2>{});
-        else run_stage(std::integral_constant<int, (UPS > 3 ? 3 : 1)>{});
-      }
-
-      const bool seg_end = sw.lo_kt == 0 || sw.hi - sw.nsub + 1 == ubeg;
-      if (!seg_end) continue;
-
-      // ---- segment end: deterministic CTA reduction (tree over warps) ----
-      float* accf = &acc[0][0][0];
-      auto red_addr = [&](int sl, int i) { return red + ((sl * C::kFrag + i) * 32 + lane) * 4u; };
-#pragma unroll
-      for (int half = CW / 2; half >= 1; half >>= 1) {
-        if (warp >= half && warp < 2 * half) {
-#pragma unroll
-          for (int i = 0; i < C::kFrag; ++i)
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_addr(warp - half, i)), "f"(accf[i]));
-        }
-        named_bar_sync(1, kConsumerWarps * 32);
-        if (warp < half) {
-#pragma unroll
-          for (int i = 0; i < C::kFrag; ++i) {
-            float v;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(red_addr(warp, i)));
-            accf[i] += v;
+        if (sw.nsub == 2) {
+          run_stage(std::integral_constant<int, 2>{});
+        } else if constexpr (UPS > 3) {
+          if (sw.nsub == 3) {
+            run_stage(std::integral_constant<int, 3>{});
+          } else if constexpr (UPS > 4) {
+            // UPS = 8: 4..7 sub-units
+            if (sw.nsub == 4) run_stage(std::integral_constant<int, 4>{});
+            else if (sw.nsub == 5) run_stage(std::integral_constant<int, 5>{});
+            else if (sw.nsub == 6) run_stage(std::integral_constant<int, 6>{});
+            else run_stage(std::integral_constant<int, (UPS > 7 ? 7 : 1)>{});
           }
         }
-        named_bar_sync(1, kConsumerWarps * 32);
       }
-
-      const int tile = sw.tile;
-      const bool last_seg = sw.hi - sw.nsub + 1 == ubeg;
-      if (threadIdx.x == 0) FLUTE_STAMP(last_seg ? 5 : 4);
-      if (warp == 0) {
-        const int t0 = tile * tiles_k;
-        const bool started = ubeg <= t0;
-        const bool finished = uend >= t0 + tiles_k;
-        if (!finished) {
-          // contributor: publish the fp32 partial, then release-add the
-          // finisher's flag.
-          float* my_slot = p.slots + static_cast<size_t>(wid) * C::kFrag * 32;
+#ifdef FLUTE_DIAGNOSTICS
+      if (trace) {
+        // make the timestamp wait for this warp's MMAs to retire
+        float sink = 0.f;
 #pragma unroll
-          for (int i = 0; i < C::kFrag; ++i) my_slot[i * 32 + lane] = accf[i];
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) red_release_gpu_add(p.flags + owner_of(t0 + tiles_k - 1, U, P), 1u);
-        } else {
-          if (!started) {
-            // finisher: contributors = non-empty workers in [owner(t0), wid)
-            const int first = owner_of(t0, U, P);
-            uint32_t expect = 0;
-            for (int c = first; c < wid; ++c)
-              expect += range_lo(c + 1, U, P) > range_lo(c, U, P) ? 1u : 0u;
-            while (ld_acquire_gpu(p.flags + wid) < expect) {
-            }
-            if (threadIdx.x == 0) FLUTE_STAMP(7);
-            // ((c_first + c_next) + ...) + own
-            float sum[C::kFrag];
-            bool have = false;
-            for (int c = first; c < wid; ++c) {
-              if (range_lo(c + 1, U, P) <= range_lo(c, U, P)) continue;
-              const float* src = p.slots + static_cast<size_t>(c) * C::kFrag * 32 + lane;
-              if (!have) {
-#pragma unroll
-                for (int i = 0; i < C::kFrag; ++i) sum[i] = __ldcg(src + i * 32);
-              } else {
-#pragma unroll
-                for (int i = 0; i < C::kFrag; ++i) sum[i] += __ldcg(src + i * 32);
-              }
-              have = true;
-            }
-#pragma unroll
-            for (int i = 0; i < C::kFrag; ++i) accf[i] = sum[i] + accf[i];
-            __syncwarp();
-            if (lane == 0) *reinterpret_cast<volatile uint32_t*>(p.flags + wid) = 0u;
-          }
-          // write Y (f16, RNE)
-          const int g = lane >> 2, t = lane & 3;
-          const int ncol0 = tile * kUnitN;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int r = 0; r < 4; ++r) {
-                const int row = mt * 8 + 2 * t + (r & 1);
-                const int col = ncol0 + 16 * j + g + 8 * (r >> 1);
-                if (row < p.m && col < p.n)
-                  p.y[static_cast<size_t>(row) * p.n + col] = __float2half_rn(acc[mt][j][r]);
-              }
-        }
+        for (int mt = 0; mt < MT; ++mt) sink += acc[mt][0][0] + acc[mt][3][3];
+        trace[2] = gtimer() + (sink == 1.2345e-30f ? 1 : 0);
       }
+      ++stage_no;
+#endif
+      if (!sw.seg_end(ubeg)) continue;
+      // ---- segment end: park the partial for the epilogue warp ----
+      if (seg > 0) mbar_wait(epi_empty, (seg - 1) & 1);
+      const float* accf = &acc[0][0][0];
+#pragma unroll
+      for (int i = 0; i < C::kFrag; ++i)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(part + ((warp * C::kFrag + i) * 32 + lane) * 4u),
+                     "f"(accf[i]));
+      mbar_arrive(epi_full);
+      ++seg;
     }
   }
 

@@ -106,8 +106,11 @@ const DevProps& props() {
   return pr;
 }
 
-// FLUTE_DEBUG_TIMES=1: per-CTA %globaltimer stamps {start, producer issued,
-// LUT ready, first stage ready, first segment end, last segment end, exit}.
+// FLUTE_DEBUG_TIMES=1 (diag build): per-CTA %globaltimer stamps {start,
+// producer issued, LUT ready, first stage ready, segment end, last segment
+// end, exit, finisher acquired} followed by a per-stage trace of consumer
+// warp 0: 64 stages x {wait begin, data ready, compute done}.
+constexpr size_t kDbgPerCta = 8 + 64 * 3;
 unsigned long long* g_dbg = nullptr;
 int g_dbg_cap = 0;
 unsigned long long* debug_times_buffer(int workers) {
@@ -115,50 +118,41 @@ unsigned long long* debug_times_buffer(int workers) {
   if (!on) return nullptr;
   if (g_dbg_cap < workers) {
     if (g_dbg) cudaFree(g_dbg);
-    FLUTE_CUDA(cudaMalloc(&g_dbg, static_cast<size_t>(workers) * 8 * 8));
+    FLUTE_CUDA(cudaMalloc(&g_dbg, static_cast<size_t>(workers) * kDbgPerCta * 8));
     g_dbg_cap = workers;
   }
-  FLUTE_CUDA(cudaMemset(g_dbg, 0, static_cast<size_t>(workers) * 8 * 8));
+  FLUTE_CUDA(cudaMemset(g_dbg, 0, static_cast<size_t>(workers) * kDbgPerCta * 8));
   return g_dbg;
 }
 
 int bm_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : 32; }
 
-template <int BITS, int BM, int UPS, int CW>
+template <int BITS, int BM, int UPS>
 int stages_for() {
   const size_t cap = props().smem_optin;
   int s = kMaxStages;
-  while (s > 2 && Cfg<BITS, BM, UPS, CW>::smem_bytes(s) > cap) --s;
+  while (s > 2 && Cfg<BITS, BM, UPS>::smem_bytes(s) > cap) --s;
   return s;
 }
 
-// Consumer warps: 16 (4 per SM sub-partition) while the accumulators are
-// small enough for the ~100-register budget of 544 threads; 8 for m > 16.
-template <int BM>
-constexpr int cw_for() {
-  return 8;
-}
-
-// Sub-units per stage: 4 (512-deep stages) for m <= 16; 2 for m <= 32 where
-// the X slice of a stage is 4x larger.
+// Sub-units per stage (stage depth 128*UPS in k): 8 for m <= 8, 4 for m <= 16,
+// 2 for m <= 32 where a stage's X slice is 4x larger (smem-limited).
 template <int BM>
 constexpr int ups_for() {
-  return BM == 32 ? 2 : 4;
+  return BM == 8 ? 8 : BM == 16 ? 4 : 2;
 }
 
-template <int BITS, int BM>
+template <int BITS, int BM, int UPS>
 void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp) {
-  constexpr int UPS = ups_for<BM>();
-  constexpr int CW = cw_for<BM>();
-  using Cf = Cfg<BITS, BM, UPS, CW>;
+  using Cf = Cfg<BITS, BM, UPS>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   FLUTE_CUDA(cudaGetDevice(&dev));
-  const int S = stages_for<BITS, BM, UPS, CW>();
+  const int S = stages_for<BITS, BM, UPS>();
   const size_t smem = Cf::smem_bytes(S);
   if (configured_dev != dev) {
-    FLUTE_CUDA(cudaFuncSetAttribute(qgemm_mma_kernel<BITS, BM, UPS, CW>,
+    FLUTE_CUDA(cudaFuncSetAttribute(qgemm_mma_kernel<BITS, BM, UPS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
     configured_dev = dev;
@@ -192,24 +186,39 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(workers));
-  cfg.blockDim = dim3(threads_for<CW>());
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = static_cast<cudaStream_t>(a.stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  FLUTE_CUDA(cudaLaunchKernelEx(&cfg, qgemm_mma_kernel<BITS, BM, UPS, CW>, map, kp));
+  static const bool no_pdl = std::getenv("FLUTE_NO_PDL") != nullptr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  FLUTE_CUDA(cudaLaunchKernelEx(&cfg, qgemm_mma_kernel<BITS, BM, UPS>, map, kp));
 }
 
 template <int BITS>
 void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp) {
   switch (bm_for(m_rows)) {
-    case 8: launch_impl<BITS, 8>(a, m_rows, x, y, workers, units, tiles_k, gp); break;
-    case 16: launch_impl<BITS, 16>(a, m_rows, x, y, workers, units, tiles_k, gp); break;
-    default: launch_impl<BITS, 32>(a, m_rows, x, y, workers, units, tiles_k, gp); break;
+    case 8: {
+#ifdef FLUTE_VARIANTS
+      // Tuning sweep (make diag): FLUTE_VARIANT = sub-units per stage.
+      static const char* v = std::getenv("FLUTE_VARIANT");
+      const std::string vs = v ? v : "";
+      if (vs == "2") return launch_impl<BITS, 8, 2>(a, m_rows, x, y, workers, units, tiles_k, gp);
+      if (vs == "4") return launch_impl<BITS, 8, 4>(a, m_rows, x, y, workers, units, tiles_k, gp);
+#endif
+      launch_impl<BITS, 8, ups_for<8>()>(a, m_rows, x, y, workers, units, tiles_k, gp);
+      break;
+    }
+    case 16:
+      launch_impl<BITS, 16, ups_for<16>()>(a, m_rows, x, y, workers, units, tiles_k, gp);
+      break;
+    default:
+      launch_impl<BITS, 32, ups_for<32>()>(a, m_rows, x, y, workers, units, tiles_k, gp);
+      break;
   }
 }
 
@@ -242,7 +251,7 @@ int default_workers(int m, int k, int n, int bits) {
 
 void debug_times(unsigned long long* out, int workers) {
   if (!g_dbg) throw flutesim::InputError("FLUTE_DEBUG_TIMES not enabled");
-  FLUTE_CUDA(cudaMemcpy(out, g_dbg, static_cast<size_t>(std::min(workers, g_dbg_cap)) * 64,
+  FLUTE_CUDA(cudaMemcpy(out, g_dbg, static_cast<size_t>(std::min(workers, g_dbg_cap)) * kDbgPerCta * 8,
                         cudaMemcpyDeviceToHost));
 }
 
