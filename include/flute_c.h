@@ -124,6 +124,19 @@ int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int work
 int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
                     int workers, void* stream);
 
+/* The reference call itself: flutesim::execute (engine.hpp:72, engine.cpp:345)
+ * on HOST buffers in the reference's canonical formats — x f16 [m][k],
+ * canonical slices from reorder_and_split at `layout`, scales f16 [n][k/g],
+ * the make_vectorized_lut table (2^(2b)*dup words) — run on the GPU.  y:
+ * f16 [m][n]; stats (nullable): the 7 TrafficStats fields of the reference
+ * accounting model (== flute_plan_traffic for the same shape).  workers = the
+ * Stream-K CTA count (the reference's simulated SMs); stages / tile_m are
+ * validated as the reference does and never change results. */
+int flute_execute(const uint16_t* x, int m, const uint32_t* slice_hi, const uint32_t* slice_lo,
+                  int k, int n, int bits, int group, const int* layout, const uint16_t* scales,
+                  const uint32_t* vlut_words, int dup, int workers, int stages, int tile_m,
+                  uint16_t* y, uint64_t* stats);
+
 /* ---- device self-checks (used by the parity tests) ----------------------- */
 /* Run the kernel's own dequant routine over every pair x every scale:
  * out[s * 2^(2b) + p] = device half2 for (pair p, scales[s]); pair p in

@@ -106,6 +106,9 @@ class DeviceWeights {
   void gemm(const Half* x_dev, int m, Half* y_dev, int workers = 0, void* stream = nullptr);
   // Host in / host out (copies inside; synchronizes the stream).
   MatH gemm_host(const MatH& x, int workers = 0, void* stream = nullptr);
+  // Raw host buffers (f16 bits; pinned memory makes the copies truly async).
+  void gemm_host_raw(const std::uint16_t* x_host, int m, std::uint16_t* y_host, int workers = 0,
+                     void* stream = nullptr);
 
   struct Impl;
 

@@ -120,6 +120,9 @@ _SIGS = {
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "flute_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _vp]),
     "flute_gemm_host": (C.c_int, [_vp, _u16p, C.c_int, _u16p, C.c_int, _vp]),
+    "flute_execute": (C.c_int, [_u16p, C.c_int, _u32p, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                _i32p, _u16p, _u32p, C.c_int, C.c_int, C.c_int, C.c_int, _u16p,
+                                _u64p]),
     "flute_dequant_all_device": (C.c_int, [_u32p, C.c_int, _u16p, C.c_int, _u32p]),
     "flute_mma_fragment": (C.c_int, [_u16p, _u16p, _f32p, C.c_int, C.c_int, C.c_int]),
     "flute_debug_times": (C.c_int, [_u64p, C.c_int]),
@@ -416,6 +419,31 @@ def qgemm(x, w_dev, scales_dev, vlut_dev, bits: int, group: int, n: int, workspa
                             workspace.numel() * workspace.element_size(), workers,
                             _stream_ptr(stream)))
     return y
+
+
+@dataclass
+class MatmulResult:
+    y: np.ndarray          # f16 bits [m][n]
+    stats: dict            # TrafficStats (reference accounting model)
+
+
+def execute(x16: np.ndarray, slices, k: int, n: int, bits: int, group: int, scales: np.ndarray,
+            vlut_words: np.ndarray, dup: int = 1, layout=DEFAULT_LAYOUT, workers: int = 1,
+            stages: int = 2, tile_m: int = 0) -> MatmulResult:
+    """engine.hpp:72 ``execute(MatmulProblem)`` on the GPU: canonical slices
+    (reorder_and_split), [n][k/g] scales and a make_vectorized_lut table, all
+    host arrays; returns y (f16 bits) and the reference TrafficStats."""
+    x16 = np.ascontiguousarray(x16, np.uint16)
+    m = x16.shape[0]
+    hi = np.ascontiguousarray(slices[0], np.uint32)
+    lo = np.ascontiguousarray(slices[1], np.uint32) if bits == 3 else None
+    y = np.zeros((m, n), np.uint16)
+    st = np.zeros(7, np.uint64)
+    _check(_lib.flute_execute(x16, m, hi, lo.ctypes.data if lo is not None else None, k, n, bits,
+                              group, _lay(layout), np.ascontiguousarray(scales, np.uint16),
+                              np.ascontiguousarray(vlut_words, np.uint32), dup, workers, stages,
+                              tile_m, y, st))
+    return MatmulResult(y, dict(zip(TRAFFIC_FIELDS, (int(v) for v in st))))
 
 
 def dequant_all_device(vlut_words: np.ndarray, bits: int, scales: np.ndarray) -> np.ndarray:

@@ -1,6 +1,7 @@
 // flute-b200 — C ABI implementation (include/flute_c.h).  Thin: every entry
 // point converts plain pointers to the C++ API and maps exceptions to status
 // codes, keeping the message for flute_last_error().
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -438,10 +439,47 @@ int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y
     need(w, "weights");
     need(x_host, "x_host");
     need(y_host, "y_host");
-    MatH x(m, w->k);
-    for (size_t i = 0; i < x.data.size(); ++i) x.data[i] = Half::from_bits(x_host[i]);
-    const MatH y = w->impl->gemm_host(x, workers, stream);
-    for (size_t i = 0; i < y.data.size(); ++i) y_host[i] = y.data[i].bits;
+    w->impl->gemm_host_raw(x_host, m, y_host, workers, stream);
+  });
+}
+
+int flute_execute(const uint16_t* x, int m, const uint32_t* slice_hi, const uint32_t* slice_lo,
+                  int k, int n, int bits, int group, const int* layout, const uint16_t* scales,
+                  const uint32_t* vlut_words, int dup, int workers, int stages, int tile_m,
+                  uint16_t* y, uint64_t* stats) {
+  return guard([&] {
+    need(x, "x");
+    need(scales, "scales");
+    need(vlut_words, "vlut_words");
+    need(y, "y");
+    if (m < 1) throw ConfigError("matmul: m must be >= 1");
+    if (dup < 1) throw ConfigError("vectorized table: dup must be >= 1");
+    const PackedWeights pw = canonical_from(slice_hi, slice_lo, k, n, bits, to_layout(layout));
+    // entry e, copy 0 lives at e * dup (vec_lut.hpp:18-30)
+    std::vector<uint32_t> words(std::size_t{1} << (2 * bits));
+    for (std::size_t e = 0; e < words.size(); ++e) words[e] = vlut_words[e * dup];
+    VectorizedTable lut = table_from_words(words.data(), bits);
+    MatH xm(m, k);
+    std::memcpy(static_cast<void*>(xm.data.data()), x, xm.data.size() * 2);
+    std::vector<Half> sc(static_cast<std::size_t>(k) * n / std::max(group, 1));
+    std::memcpy(static_cast<void*>(sc.data()), scales, sc.size() * 2);
+    MatmulProblem p;
+    p.x = &xm;
+    p.weights = &pw;
+    p.scales = &sc;
+    p.lut = &lut;
+    p.cfg = QuantConfig{bits, group};
+    p.workers = workers;
+    p.stages = stages;
+    p.tile_m = tile_m;
+    const MatmulResult r = execute(p);
+    std::memcpy(y, r.y.data.data(), r.y.data.size() * 2);
+    if (stats) {
+      const TrafficStats& t = r.stats;
+      const uint64_t v[7] = {t.bytes_weights, t.bytes_scales, t.bytes_table, t.bytes_activations,
+                             t.bytes_partials_rw, t.bytes_output, t.flops};
+      std::memcpy(stats, v, sizeof v);
+    }
   });
 }
 

@@ -208,16 +208,23 @@ void DeviceWeights::gemm(const Half* x_dev, int m, Half* y_dev, int workers, voi
 
 MatH DeviceWeights::gemm_host(const MatH& x, int workers, void* stream) {
   if (x.cols != impl_->k) throw ConfigError("gemm_host: activation K does not match weight K");
-  const std::size_t xb = x.data.size() * 2;
-  const std::size_t yb = static_cast<std::size_t>(x.rows) * impl_->n * 2;
+  MatH y(x.rows, impl_->n);
+  gemm_host_raw(reinterpret_cast<const std::uint16_t*>(x.data.data()), x.rows,
+                reinterpret_cast<std::uint16_t*>(y.data.data()), workers, stream);
+  return y;
+}
+
+void DeviceWeights::gemm_host_raw(const std::uint16_t* x_host, int m, std::uint16_t* y_host,
+                                  int workers, void* stream) {
+  if (m < 1) throw ConfigError("gemm_host: m must be >= 1");
+  const std::size_t xb = static_cast<std::size_t>(m) * impl_->k * 2;
+  const std::size_t yb = static_cast<std::size_t>(m) * impl_->n * 2;
   if (impl_->xbuf.bytes < xb) impl_->xbuf = DeviceBuffer(xb);
   if (impl_->ybuf.bytes < yb) impl_->ybuf = DeviceBuffer(yb);
-  MatH y(x.rows, impl_->n);
-  flute_dev::h2d(impl_->xbuf.p, x.data.data(), xb, stream);
-  impl_->gemm(impl_->xbuf.p, x.rows, impl_->ybuf.p, workers, stream);
-  flute_dev::d2h(y.data.data(), impl_->ybuf.p, yb, stream);
+  flute_dev::h2d(impl_->xbuf.p, x_host, xb, stream);
+  impl_->gemm(impl_->xbuf.p, m, impl_->ybuf.p, workers, stream);
+  flute_dev::d2h(y_host, impl_->ybuf.p, yb, stream);
   flute_dev::stream_sync(stream);
-  return y;
 }
 
 // ---------------------------------------------------------------------------

@@ -107,14 +107,14 @@ int main() {
       {1, 6, 32768, 1, 8},  {1, 8, 16384, 4, 8},  {2, 6, 16384, 1, 8},  {2, 12, 8192, 1, 8},
       {4, 6, 8192, 1, 4},   {1, 8, 16384, 1, 1},  {1, 8, 16384, 1, 16},
   };
-  printf("ctas/sm stages chunk copies cons  |  GB/s (1 GiB stream)   |  GB/s (23 MB per launch)\n");
+  printf("ctas/sm stages chunk copies cons  |  GB/s (1 GiB stream)   |  GB/s (23 MB per launch) | GB/s (8.5 MB per launch)\n");
   for (const Cfg& c : cfgs) {
     const int grid = sms * c.ctas_per_sm;
     const size_t smem = size_t(c.S) * c.chunk + 16 * c.S + 64;
     cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    double gbs[2];
-    for (int mode = 0; mode < 2; ++mode) {
-      const size_t bytes = mode == 0 ? total : size_t(23) << 20;
+    double gbs[3];
+    for (int mode = 0; mode < 3; ++mode) {
+      const size_t bytes = mode == 0 ? total : mode == 1 ? size_t(23) << 20 : size_t(17) << 19;
       size_t per_cta = bytes / grid / c.chunk * c.chunk;
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
@@ -136,8 +136,8 @@ int main() {
       cudaError_t err = cudaGetLastError();
       if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
     }
-    printf("%7d %6d %6u %6d %4d  |  %8.0f               |  %8.0f\n", c.ctas_per_sm, c.S, c.chunk,
-           c.copies, c.ncons, gbs[0], gbs[1]);
+    printf("%7d %6d %6u %6d %4d  |  %8.0f               |  %8.0f  |  %8.0f\n", c.ctas_per_sm, c.S,
+           c.chunk, c.copies, c.ncons, gbs[0], gbs[1], gbs[2]);
   }
   return 0;
 }
