@@ -3,33 +3,33 @@
 //
 // Reference semantics: flutesim::execute (engine.cpp:345) — Y = X * W_hat with
 // W_hat = f16(scale * T[index]) (vec_lut.cpp:39-48) and fp32 accumulation;
-// Stream-K ranges [floor(w*U/P), floor((w+1)*U/P)) over 128-deep sub-units
+// Stream-K ranges [floor(w*U/P), floor((w+1)*U/P)) over 128-deep units
 // (n-tile major, k inner; streamk.cpp:17-58) with a fixed-order fixup of split
 // tiles (engine.cpp:279-333).
 //
 // One CTA = one Stream-K worker = 8 consumer warps + 1 producer warp + 1
-// epilogue warp, all synchronised through mbarriers only (no CTA barrier in
-// the steady state):
-//  * Producer.  Walks the CTA's sub-units in descending order, grouping up to
-//    UPS consecutive sub-units of one 64-column tile into a stage: weights and
-//    scales are contiguous in the device layout (one 1-D bulk copy each,
-//    UBLKCP) and the X slice is one 3-D TMA box {64 k, m rows, 2*UPS chunks},
-//    128B-swizzled (UTMALDG).  The weight/scale copies of the first S stages
-//    are issued before the programmatic-dependent-launch wait, so they overlap
-//    the previous kernel in the stream.
-//  * Consumer warp w owns k-step w of every sub-unit: LDS of its packed pair
-//    indices, PRMT -> LDS from the 32-way duplicated vLUT, HMUL2 by the group
-//    scale (operand-selector broadcast), mma.sync m16n8k16 with W^T as the A
-//    operand (HMMA.16816.F32), X^T fragments via ldmatrix.  At the end of an
-//    output-tile segment it parks its fp32 partial in shared memory, arrives
-//    on `epi_full` and goes straight on with the next stage.
+// epilogue warp, synchronised through mbarriers only (no CTA barrier in the
+// steady state).  Every role walks the CTA's range the same way: tiles
+// (segments) in descending order, and inside a tile stages of UPS units from
+// the top k-slice down, so only a segment's last stage can be short.
+//  * Producer.  Per stage: one 1-D bulk copy (UBLKCP) of the weights (a stage
+//    is contiguous in the device layout), one of the group scales, and one
+//    3-D TMA box (UTMALDG, 128B swizzle) of the X slice.  The weight/scale
+//    copies of the first S stages are issued before the programmatic-
+//    dependent-launch wait, so they overlap the previous kernel in the stream
+//    (OCC = 2 configurations leave room for that CTA to be co-resident).
+//  * Consumer warp w owns k-step w (16 deep) of every unit: LDS of its packed
+//    pair indices, PRMT -> LDS from the 32-way duplicated vLUT, HMUL2 by the
+//    group scale (operand-selector broadcast), mma.sync m16n8k16 with W^T as
+//    the A operand (HMMA.16816.F32), X^T fragments via ldmatrix.  At the end
+//    of a segment it parks its fp32 partial in shared memory and goes on.
 //  * Epilogue warp.  Sums the 8 warp partials in fixed order (deterministic),
-//    releases the buffer (`epi_empty`), then does the Stream-K fixup off the
-//    critical path: contributors publish their fp32 partial and release-add
-//    the finisher's flag; finishers acquire, add contributors in ascending
-//    worker (= ascending k) order, add their own partial, write Y and re-arm
-//    their flag (graph / back-to-back safe).  The descending walk processes a
-//    split tile's contributor segment first, so finishers rarely wait.
+//    then does the Stream-K fixup off the critical path: contributors publish
+//    their fp32 partial and release-add the finisher's flag; finishers
+//    acquire, add contributors in ascending worker (= ascending k) order, add
+//    their own partial, write Y and re-arm their flag (graph / back-to-back
+//    safe).  The descending walk processes a split tile's contributor segment
+//    first, so finishers rarely wait.
 #pragma once
 
 #include <cuda.h>
@@ -48,7 +48,7 @@ constexpr int kEpilogueWarp = kConsumerWarps + 1;
 constexpr int kThreads = 32 * (kConsumerWarps + 2);
 constexpr int kMaxStages = 16;
 constexpr int kUnitN = 64;   // == flutesim::kUnitN (pack.hpp)
-constexpr int kUnitK = 128;  // == flutesim::kUnitK: one Stream-K sub-unit
+constexpr int kUnitK = 128;  // == flutesim::kUnitK: one Stream-K unit
 
 struct KParams {
   const uint8_t* w;
@@ -58,32 +58,51 @@ struct KParams {
   float* slots;
   uint32_t* flags;
   int m, n;
-  int tiles_k;      // sub-units per 64-column tile
+  int tiles_k;      // units per 64-column tile
   int group_shift;  // log2(group size)
   int gp;           // padded groups per column
-  int units;        // total sub-units
+  int units;        // total units
   int workers;
   int stages;
   int use_ticket;
   int x3d;   // X tensor map is the 3-D {64, m, k/64} view (k % 64 == 0)
+  // shared-memory plan (host: plan_smem in qgemm_mma.cu), byte offsets
+  uint32_t part_off;      // partial rows that do not fit in the vLUT row gaps
+  uint32_t part_stride;   // (unused by the device; kept for the host plan)
+  uint32_t stage_off;     // first stage (1024-aligned)
+  uint32_t stage_bytes;   // stage stride (multiple of 1024): [X | W | scales]
+  uint32_t x_bytes;       // X region of a stage (1024-aligned; last 128 B = zero row)
+  uint32_t bar_off;
+  // Cluster split-K mode (cluster > 1): cluster c = 64-column tile c, its
+  // `cluster` CTAs split the tile's k-units evenly and reduce through
+  // distributed shared memory into rank 0 (receive buffer at recv_off).
+  int cluster;
+  uint32_t recv_off;
   int diag;  // FLUTE_DIAG bits (diag build only; results are wrong when set):
-             // 1 skip dequant/MMA, 2 skip weight loads, 4 skip X, 8 skip scales
+             // 1 skip dequant/MMA, 2 skip weight loads, 4 skip X, 8 skip scales,
+             // 16 skip the Stream-K fixup, 32 skip the vLUT fill, 64 skip Y
   unsigned long long* dbg;  // per-CTA timeline (diag build, FLUTE_DEBUG_TIMES)
 };
 
 template <int BITS, int BM, int UPS>
 struct Cfg {
-  static constexpr int kLutBytes = (1 << (2 * BITS)) * kLutRowBytes;
+  static constexpr int kEntries = 1 << (2 * BITS);
+  static constexpr int kLutBytes = kEntries * kLutRowBytes;
   static constexpr int kSubBytes = BITS * 1024;  // 64 x 128 weights
-  static constexpr int kXBytes = 2 * UPS * BM * 128;
   static constexpr int kWBytes = UPS * kSubBytes;
-  static constexpr int kScBytes = UPS * 4 * 128;  // <= 4 groups per sub-unit
-  static constexpr int kFrag = (BM / 8) * 16;     // accumulator floats / lane
-  static constexpr int kPartBytes = kConsumerWarps * kFrag * 32 * 4;
-  static constexpr int kStageBytes = kXBytes + kWBytes + kScBytes;
-  static constexpr size_t smem_bytes(int S) {
-    return static_cast<size_t>(kLutBytes) + static_cast<size_t>(S) * kStageBytes + kPartBytes +
-           8 * (2 * kMaxStages + 2) + 64;
+  static constexpr int kFrag = (BM / 8) * 16;  // accumulator floats / lane
+  static constexpr int kPartRows = kConsumerWarps * kFrag;
+  // The vLUT uses the low 128 bytes of each 256-byte row (lane copies); the
+  // first kPartRowsInLut partial-sum rows live in the high halves (a whole
+  // number of warps' rows), the rest in a separate 128-byte-row buffer.
+  static constexpr int kPartRowsInLut =
+      (kPartRows < kEntries ? kPartRows : kEntries) / kFrag * kFrag;
+  static constexpr int kPartBytes = (kPartRows - kPartRowsInLut) * 128;
+  static constexpr int kBarBytes = 8 * (2 * kMaxStages + 2) + 64;
+  // shared address (before + lane*4) of partial row r (part = separate buffer)
+  static __device__ __forceinline__ uint32_t part_row(uint32_t lut, uint32_t part, int r) {
+    return r < kPartRowsInLut ? lut + r * kLutRowBytes + kLutRowBytes / 2
+                              : part + (r - kPartRowsInLut) * 128;
   }
 };
 
@@ -122,39 +141,41 @@ __device__ __forceinline__ int owner_of(int x, int U, int P) {
   return w;
 }
 
-// Descending walk over a CTA range in stages of <= UPS sub-units that never
-// cross a tile boundary.  Producer, consumers and the epilogue warp run
-// identical copies.
-template <int UPS>
-struct StageWalk {
-  int hi, tile, kt;  // highest remaining sub-unit, its tile and k-slice
-  int nsub, lo_kt;   // current stage: sub-units [hi-nsub+1, hi], k-slices [lo_kt, kt]
-  __device__ __forceinline__ void init(int uend, int tiles_k) {
-    hi = uend - 1;
-    tile = hi / tiles_k;
-    kt = hi - tile * tiles_k;
+// The CTA's range [ubeg, uend) as segments (one per tile, descending); a
+// segment covers k-slices [kt_bot, kt_top] of tile t.
+struct SegRange {
+  int t_hi, t_lo, ubeg, uend, tiles_k;
+  __device__ __forceinline__ void init(int ub, int ue, int tk) {
+    ubeg = ub;
+    uend = ue;
+    tiles_k = tk;
+    t_hi = (ue - 1) / tk;
+    t_lo = ub / tk;
   }
-  __device__ __forceinline__ void shape(int ubeg) {
-    int n = kt + 1 < UPS ? kt + 1 : UPS;
-    nsub = hi - ubeg + 1 < n ? hi - ubeg + 1 : n;
-    lo_kt = kt - nsub + 1;
+  __device__ __forceinline__ int top(int t) const {
+    return t == t_hi ? uend - 1 - t * tiles_k : tiles_k - 1;
   }
-  __device__ __forceinline__ bool seg_end(int ubeg) const {
-    return lo_kt == 0 || hi - nsub + 1 == ubeg;
-  }
-  __device__ __forceinline__ void next(int tiles_k) {
-    hi -= nsub;
-    if (lo_kt == 0) {
-      --tile;
-      kt = tiles_k - 1;
-    } else {
-      kt = lo_kt - 1;
+  __device__ __forceinline__ int bot(int t) const { return t == t_lo ? ubeg - t * tiles_k : 0; }
+};
+
+// Stage ring position (slot s, phase parity ph).
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void advance(int S) {
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
     }
   }
 };
 
-template <int BITS, int BM, int UPS>
-__global__ void __launch_bounds__(kThreads, 1)
+// OCC = CTAs per SM the register budget is sized for.  OCC = 2 lets a CTA of
+// the NEXT launch (programmatic dependent launch) co-reside with this one, so
+// its prologue and weight prefetch overlap this launch's tail; the host keeps
+// shared memory within half an SM for those configurations.
+template <int BITS, int BM, int UPS, int OCC>
+__global__ void __launch_bounds__(kThreads, OCC)
     qgemm_mma_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
   using C = Cfg<BITS, BM, UPS>;
   constexpr int MT = BM / 8;
@@ -163,16 +184,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = p.stages;
   const uint32_t base = smem_u32(smem);
   const uint32_t lut = base;
-  const uint32_t xs = base + C::kLutBytes;
-  const uint32_t ws = xs + S * C::kXBytes;
-  const uint32_t ss = ws + S * C::kWBytes;
-  const uint32_t part = ss + S * C::kScBytes;  // [warp][frag][lane] fp32 partials
-  const uint32_t bars = part + C::kPartBytes;
+  const uint32_t stages0 = base + p.stage_off;
+  const uint32_t SB = p.stage_bytes;
+  const uint32_t XB = p.x_bytes;
+  // stage s: X at stages0 + s*SB, weights at +XB, scales at +XB+kWBytes
+  auto xs_of = [&](int st) { return stages0 + st * SB; };
+  auto ws_of = [&](int st) { return stages0 + st * SB + XB; };
+  auto ss_of = [&](int st) { return stages0 + st * SB + XB + C::kWBytes; };
+  const uint32_t part = base + p.part_off;  // partial rows >= kPartRowsInLut
+  const uint32_t bars = base + p.bar_off;
   auto full = [&](int s) { return bars + 8 * s; };
   auto empty = [&](int s) { return bars + 8 * (kMaxStages + s); };
   const uint32_t epi_full = bars + 8 * (2 * kMaxStages);
   const uint32_t epi_empty = epi_full + 8;
-  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + (epi_empty + 8 - base));
+  const uint32_t recv_bar = epi_empty + 8;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + (recv_bar + 8 - base));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -181,10 +207,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     FLUTE_STAMP(0);
     for (int s = 0; s < S; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), kConsumerWarps * 32);  // every consumer thread arrives
+      mbar_init(empty(s), kConsumerWarps / 2);  // one arrive per warp of the stage's half
     }
-    mbar_init(epi_full, kConsumerWarps * 32);
-    mbar_init(epi_empty, 32);
+    mbar_init(epi_full, kConsumerWarps);
+    mbar_init(epi_empty, 1);
+    if (p.cluster > 1) mbar_init(recv_bar, 32 * (p.cluster - 1));  // every sender lane arrives
     fence_mbar_init();
   }
   int wid = blockIdx.x;
@@ -196,14 +223,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   if (p.use_ticket) wid = static_cast<int>(misc[0]);
+  // cluster mode: the receive barrier must be initialised before any peer
+  // arrives on it (waited for just before the first remote access)
+  if (p.cluster > 1) cluster_arrive_relaxed();
   pdl_launch_dependents();
 
   const int U = p.units;
   const int P = p.workers;
-  const int ubeg = range_lo(wid, U, P);
-  const int uend = range_lo(wid + 1, U, P);
   const int tiles_k = p.tiles_k;
+  int ubeg, uend;
+  uint32_t crank = 0;
+  if (p.cluster > 1) {
+    crank = cluster_ctarank();
+    const int t0c = static_cast<int>(cluster_id_x()) * tiles_k;
+    ubeg = t0c + static_cast<int>(crank) * tiles_k / p.cluster;
+    uend = t0c + (static_cast<int>(crank) + 1) * tiles_k / p.cluster;
+  } else {
+    ubeg = range_lo(wid, U, P);
+    uend = range_lo(wid + 1, U, P);
+  }
   const int gshift = p.group_shift;
+  SegRange R;
+  R.init(ubeg, uend, tiles_k);
 
   if (warp == kProducerWarp) {
     // ===================== producer =====================
@@ -214,79 +255,70 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader) prefetch_tmap(&tmap_x);
       const uint64_t pol = policy_evict_first();
       const bool do_w = !FLUTE_DIAG(2), do_x = !FLUTE_DIAG(4), do_s = !FLUTE_DIAG(8);
-      auto issue_ws = [&](const StageWalk<UPS>& sw, int s) {
-        const int glo = (sw.lo_kt * kUnitK) >> gshift;
-        const int ng = (((sw.kt + 1) * kUnitK - 1) >> gshift) - glo + 1;
-        const uint32_t xb = do_x ? (p.x3d ? 2 * UPS : 2 * sw.nsub) * p.m * 128 : 0;
-        const uint32_t wb = do_w ? sw.nsub * C::kSubBytes : 0;
+      // stage = units [t*tiles_k + lo, t*tiles_k + lo + ns) of tile t
+      auto issue_ws = [&](int t, int lo, int ns, int s) {
+        const int glo = (lo * kUnitK) >> gshift;
+        const int ng = ((((lo + ns) * kUnitK) - 1) >> gshift) - glo + 1;
+        const uint32_t xb = do_x ? (p.x3d ? 2 * UPS : 2 * ns) * p.m * 128 : 0;
+        const uint32_t wb = do_w ? ns * C::kSubBytes : 0;
         const uint32_t sb = do_s ? ng * 128 : 0;
         if (leader) {
           mbar_arrive_expect_tx(full(s), xb + wb + sb);
           if (wb)
-            bulk_g2s_hint(ws + s * C::kWBytes,
-                          p.w + static_cast<size_t>(sw.hi - sw.nsub + 1) * C::kSubBytes, wb,
-                          full(s), pol);
+            bulk_g2s_hint(ws_of(s), p.w + static_cast<size_t>(t * tiles_k + lo) * C::kSubBytes,
+                          wb, full(s), pol);
           if (sb)
-            bulk_g2s(ss + s * C::kScBytes,
-                     p.sc + (static_cast<size_t>(sw.tile) * p.gp + glo) * 128, sb, full(s));
+            bulk_g2s(ss_of(s), p.sc + (static_cast<size_t>(t) * p.gp + glo) * 128, sb, full(s));
         }
       };
-      auto issue_x = [&](const StageWalk<UPS>& sw, int s) {
+      auto issue_x = [&](int lo, int ns, int s) {
         if (!do_x || !leader) return;
         if (p.x3d) {
-          tma_3d_g2s(xs + s * C::kXBytes, &tmap_x, 0, 0, sw.lo_kt * 2, full(s));
+          tma_3d_g2s(xs_of(s), &tmap_x, 0, 0, lo * 2, full(s));
         } else {
-          for (int c = 0; c < 2 * sw.nsub; ++c)
-            tma_2d_g2s(xs + s * C::kXBytes + c * p.m * 128, &tmap_x, sw.lo_kt * kUnitK + 64 * c, 0,
-                       full(s));
+          for (int c = 0; c < 2 * ns; ++c)
+            tma_2d_g2s(xs_of(s) + c * p.m * 128, &tmap_x, lo * kUnitK + 64 * c, 0, full(s));
         }
       };
       // pass 1 (before the PDL wait): weights + scales of the first S stages
-      StageWalk<UPS> w1;
-      w1.init(uend, tiles_k);
       int pre = 0;
-      while (pre < S && w1.hi >= ubeg) {
-        w1.shape(ubeg);
-        issue_ws(w1, pre);
-        w1.next(tiles_k);
-        ++pre;
+      for (int t = R.t_hi; t >= R.t_lo && pre < S; --t) {
+        const int bot = R.bot(t);
+        for (int kt = R.top(t); kt >= bot && pre < S; kt -= UPS) {
+          const int lo = kt - UPS + 1 > bot ? kt - UPS + 1 : bot;
+          issue_ws(t, lo, kt - lo + 1, pre);
+          ++pre;
+        }
       }
       FLUTE_STAMP(1);
       if (!p.use_ticket) pdl_wait();  // X and the workspace belong to the previous kernel
-      StageWalk<UPS> w2;
-      w2.init(uend, tiles_k);
-      int s = 0;
-      uint32_t ph = 0;
-      for (int it = 0; w2.hi >= ubeg; ++it) {
-        w2.shape(ubeg);
-        if (it >= pre) {
-          mbar_wait(empty(s), ph ^ 1u);
-          issue_ws(w2, s);
-        }
-        issue_x(w2, s);
-        w2.next(tiles_k);
-        if (++s == S) {
-          s = 0;
-          ph ^= 1u;
+      Ring ring;
+      int it = 0;
+      for (int t = R.t_hi; t >= R.t_lo; --t) {
+        const int bot = R.bot(t);
+        for (int kt = R.top(t); kt >= bot; kt -= UPS, ++it) {
+          const int lo = kt - UPS + 1 > bot ? kt - UPS + 1 : bot;
+          if (it >= pre) {
+            mbar_wait(empty(ring.s), ring.ph ^ 1u);
+            issue_ws(t, lo, kt - lo + 1, ring.s);
+          }
+          issue_x(lo, kt - lo + 1, ring.s);
+          ring.advance(S);
         }
       }
     }
   } else if (warp == kEpilogueWarp) {
     // ===================== epilogue =====================
     if (!p.use_ticket) pdl_wait();  // the workspace and Y belong to the previous kernel
-    StageWalk<UPS> sw;
-    sw.init(uend, tiles_k);
     int seg = 0;
-    for (; sw.hi >= ubeg; sw.next(tiles_k)) {
-      sw.shape(ubeg);
-      if (!sw.seg_end(ubeg)) continue;
+    for (int tile = R.t_hi; uend > ubeg && tile >= R.t_lo; --tile, ++seg) {
       // fixed-order sum of the 8 warp partials, then free the buffer
       mbar_wait(epi_full, seg & 1);
       float accf[C::kFrag];
 #pragma unroll
       for (int i = 0; i < C::kFrag; ++i) {
         float v;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(part + (i * 32 + lane) * 4u));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(C::part_row(lut, part, i) + lane * 4u));
         accf[i] = v;
       }
 #pragma unroll
@@ -296,58 +328,94 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v;
           asm volatile("ld.shared.f32 %0, [%1];"
                        : "=f"(v)
-                       : "r"(part + ((w * C::kFrag + i) * 32 + lane) * 4u));
+                       : "r"(C::part_row(lut, part, w * C::kFrag + i) + lane * 4u));
           accf[i] += v;
         }
       }
-      mbar_arrive(epi_empty);
-      ++seg;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(epi_empty);
 
-      const int tile = sw.tile;
-      if (lane == 0) FLUTE_STAMP(sw.hi - sw.nsub + 1 == ubeg ? 5 : 4);
+      if (lane == 0) FLUTE_STAMP(tile == R.t_lo ? 5 : 4);
       const int t0 = tile * tiles_k;
       const bool started = ubeg <= t0;
       const bool finished = uend >= t0 + tiles_k;
-      if (!finished) {
-        // contributor: publish the fp32 partial, then release-add the
-        // finisher's flag.
-        float* my_slot = p.slots + static_cast<size_t>(wid) * C::kFrag * 32;
+      if (FLUTE_DIAG(16)) goto write_y;
+      if (p.cluster > 1) {
+        // ---- cluster split-K: ranks > 0 push their partial into rank 0's
+        // receive buffer through DSMEM; rank 0 adds them in rank order ----
+        const uint32_t recv = base + p.recv_off;
+        cluster_wait();  // every CTA has initialised its barriers
+        if (crank != 0) {
+          const uint32_t dst = mapa_shared(recv + (crank - 1) * C::kFrag * 128 + lane * 4, 0);
 #pragma unroll
-        for (int i = 0; i < C::kFrag; ++i) my_slot[i * 32 + lane] = accf[i];
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) red_release_gpu_add(p.flags + owner_of(t0 + tiles_k - 1, U, P), 1u);
+          for (int i = 0; i < C::kFrag; ++i) st_cluster_f32(dst + i * 128, accf[i]);
+          mbar_arrive_remote(mapa_shared(recv_bar, 0));
+          continue;
+        }
+        mbar_wait_cluster(recv_bar, 0);
+        for (int r = 1; r < p.cluster; ++r) {
+#pragma unroll
+          for (int i = 0; i < C::kFrag; ++i) {
+            float v;
+            asm volatile("ld.shared.f32 %0, [%1];"
+                         : "=f"(v)
+                         : "r"(recv + ((r - 1) * C::kFrag + i) * 128 + lane * 4));
+            accf[i] += v;
+          }
+        }
+        goto write_y;
+      }
+      if (!finished) {
+        // contributor: publish the fp32 partial as bit-inverted words, so an
+        // all-zero slot means "not written yet" (0xFFFFFFFF is never produced:
+        // NaNs are canonicalised to 0x7FFFFFFF).  No flag, no fence: the
+        // finisher polls the data itself.
+        // (volatile = relaxed, system scope: straight to L2, immediate offsets)
+        volatile uint32_t* my_slot =
+            reinterpret_cast<volatile uint32_t*>(p.slots) + static_cast<size_t>(wid) * C::kFrag * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < C::kFrag; ++i) {
+          uint32_t b = __float_as_uint(accf[i]);
+          if (b == 0xFFFFFFFFu) b = 0x7FFFFFFFu;
+          my_slot[i * 32] = ~b;
+        }
         continue;
       }
       if (!started) {
-        // finisher: contributors = non-empty workers in [owner(t0), wid)
+        // finisher: contributors = non-empty workers in [owner(t0), wid), added
+        // to the own partial in ascending worker (= ascending k) order:
+        // ((own + c_first) + c_next) + ...  — a fixed order, so results are
+        // bitwise reproducible for a given worker count.
         const int first = owner_of(t0, U, P);
-        uint32_t expect = 0;
-        for (int c = first; c < wid; ++c)
-          expect += range_lo(c + 1, U, P) > range_lo(c, U, P) ? 1u : 0u;
-        while (ld_acquire_gpu(p.flags + wid) < expect) {
-        }
-        if (lane == 0) FLUTE_STAMP(7);
-        // ((c_first + c_next) + ...) + own
-        float sum[C::kFrag];
-        bool have = false;
         for (int c = first; c < wid; ++c) {
           if (range_lo(c + 1, U, P) <= range_lo(c, U, P)) continue;
-          const float* src = p.slots + static_cast<size_t>(c) * C::kFrag * 32 + lane;
-          if (!have) {
+          volatile uint32_t* src =
+              reinterpret_cast<volatile uint32_t*>(p.slots) + static_cast<size_t>(c) * C::kFrag * 32 + lane;
+          // poll in chunks of 16 words (bounded registers), all loads of a
+          // chunk in flight together
 #pragma unroll
-            for (int i = 0; i < C::kFrag; ++i) sum[i] = __ldcg(src + i * 32);
-          } else {
+          for (int i0 = 0; i0 < C::kFrag; i0 += 16) {
+            uint32_t v[16];
+            bool ready;
+            do {
+              ready = true;
 #pragma unroll
-            for (int i = 0; i < C::kFrag; ++i) sum[i] += __ldcg(src + i * 32);
+              for (int i = 0; i < 16; ++i) {
+                v[i] = src[(i0 + i) * 32];
+                ready &= v[i] != 0u;
+              }
+            } while (!ready);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              accf[i0 + i] += __uint_as_float(~v[i]);
+              src[(i0 + i) * 32] = 0u;  // re-arm (graph / back-to-back safe)
+            }
           }
-          have = true;
         }
-#pragma unroll
-        for (int i = 0; i < C::kFrag; ++i) accf[i] = sum[i] + accf[i];
-        __syncwarp();
-        if (lane == 0) *reinterpret_cast<volatile uint32_t*>(p.flags + wid) = 0u;
+        if (lane == 0) FLUTE_STAMP(7);
       }
+    write_y:
+      if (FLUTE_DIAG(64)) continue;
       // write Y (f16, RNE); accf[(mt*4 + j)*4 + r] is C[n][m] of atom j, m-tile mt
       const int g = lane >> 2, t = lane & 3;
       const int ncol0 = tile * kUnitN;
@@ -365,164 +433,211 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== consumers =====================
-    fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
+    if (!FLUTE_DIAG(32)) fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
-    const int kstep = warp;  // 16-deep k step within a sub-unit
+    // Two halves of 4 warps take alternate stages (half h: stages i with
+    // i % 2 == h), so the two warps sharing an SMSP are out of phase (one in
+    // its LUT-lookup phase while the other issues MMAs).  Warp q of a half
+    // owns k-steps 2q and 2q+1 (16 deep each) of every unit of its stages.
+    const int half = warp >> 2;
+    const int q4 = warp & 3;
+    constexpr int KS = 2;  // k-steps per warp per unit
     // X stage = TMA box {64 k, m rows, 2*UPS chunks}, compact ([chunk][m][128 B],
-    // 128B-swizzled by box row R = chunk*m + row).  ldmatrix lanes whose row is
-    // >= m read the stage buffer's last 128 bytes, which TMA never writes when
+    // 128B-swizzled by box row Rw = chunk*m + row).  ldmatrix lanes whose row is
+    // >= m read the X region's last 128 bytes, which TMA never writes when
     // m < BM and which are zeroed here — so no zero-fill bytes move.
-    constexpr int XQ = MT > 1 ? MT / 2 : 1;
-    uint32_t xoff[UPS][XQ];  // per sub-unit r, per ldmatrix: byte offset in a stage
+    // MT == 1: one ldmatrix.x4 per unit covers both k-steps (b0, b1 of each);
+    // MT >= 2: per k-step, one ldmatrix.x4 per pair of m-tiles.
+    constexpr int XL = MT == 1 ? 1 : KS * (MT / 2);
+    uint32_t xoff[UPS][XL];
     {
       const int mrows = p.m;
+      const int mat = lane >> 3;
 #pragma unroll
-      for (int q = 0; q < XQ; ++q) {
-        const int mat = lane >> 3;
-        const int row = MT == 1 ? (lane & 7) : q * 16 + (mat >> 1) * 8 + (lane & 7);
-        const int col = (kstep & 3) * 2 + (MT == 1 ? ((lane >> 3) & 1) : (mat & 1));
+      for (int xl = 0; xl < XL; ++xl) {
+        int row, ks, colh;
+        if (MT == 1) {
+          ks = mat >> 1;
+          colh = mat & 1;
+          row = lane & 7;
+        } else {
+          constexpr int MH = MT / 2 > 0 ? MT / 2 : 1;
+          ks = xl / MH;
+          const int qq = xl % MH;
+          colh = mat & 1;
+          row = qq * 16 + (mat >> 1) * 8 + (lane & 7);
+        }
+        const int kstep = 2 * q4 + ks;
+        const int col = (kstep & 3) * 2 + colh;
 #pragma unroll
         for (int r = 0; r < UPS; ++r) {
-          const int R = (2 * r + (kstep >> 2)) * mrows + row;
-          xoff[r][q] = row < mrows ? static_cast<uint32_t>(R * 128 + ((col ^ (R & 7)) << 4))
-                                   : static_cast<uint32_t>(C::kXBytes - 128);
+          const int Rw = (2 * r + (kstep >> 2)) * mrows + row;
+          xoff[r][xl] = row < mrows ? static_cast<uint32_t>(Rw * 128 + ((col ^ (Rw & 7)) << 4))
+                                    : XB - 128u;
         }
       }
       if (mrows < BM) {
         for (int i = threadIdx.x; i < S * 8; i += kConsumerWarps * 32)
           asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
-                           xs + (i >> 3) * C::kXBytes + C::kXBytes - 128 + (i & 7) * 16),
+                           xs_of(i >> 3) + XB - 128 + (i & 7) * 16),
                        "r"(0u));
       }
     }
     named_bar_sync(1, kConsumerWarps * 32);  // LUT + zero rows visible
     if (threadIdx.x == 0) FLUTE_STAMP(2);
 
+    // this lane's bytes within a unit for k-step ks: W4 16 B at slot*16; W2
+    // 8 B at slot*8; W3 8 B (2-bit plane) at slot*8 + 4 B (1-bit plane) at
+    // 2048 + slot*4, slot = kstep*32 + lane
+    const int slot0 = 2 * q4 * 32 + lane;
+    const uint32_t w_lane = slot0 * (BITS == 4 ? 16 : 8);
+    constexpr uint32_t kSlotStride = 32 * (BITS == 4 ? 16 : 8);  // next k-step
+    const uint32_t s_lane = (lane >> 2) * 16;
+    const int kw = 32 * q4;  // k offset of this warp's first k-step in a unit
+
     float acc[MT][4][4];
-    StageWalk<UPS> sw;
-    sw.init(uend, tiles_k);
-    int s = 0, seg = 0;
-    uint32_t ph = 0;
-    bool first_stage = true;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[mt][j][r] = 0.f;
+    Ring ring;  // position of the global stage counter
 #ifdef FLUTE_DIAGNOSTICS
+    // per-stage trace of consumer warp 0: {wait begin, data ready, compute done}
     int stage_no = 0;
+    unsigned long long* trace =
+        (p.dbg && threadIdx.x == 0)
+            ? p.dbg + static_cast<size_t>(gridDim.x) * 8 + static_cast<size_t>(blockIdx.x) * 64 * 3
+            : nullptr;
 #endif
-    for (; sw.hi >= ubeg; sw.next(tiles_k), s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u) {
-      sw.shape(ubeg);
-      if (first_stage || sw.kt == tiles_k - 1) {
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[mt][j][r] = 0.f;
-      }
+
+    // One stage of NS units [lo, lo + NS) in ring slot (s, ph).
+    auto run_stage = [&](auto ns_tag, int lo, int s, uint32_t ph) {
+      constexpr int NS = decltype(ns_tag)::value;
 #ifdef FLUTE_DIAGNOSTICS
-      // per-stage trace of consumer warp 0: {wait begin, data ready, compute done}
-      unsigned long long* trace =
-          (p.dbg && threadIdx.x == 0 && stage_no < 60)
-              ? p.dbg + static_cast<size_t>(gridDim.x) * 8 +
-                    (static_cast<size_t>(blockIdx.x) * 64 + stage_no) * 3
-              : nullptr;
-      if (trace) trace[0] = gtimer();
+      if (trace && stage_no < 64) trace[stage_no * 3] = gtimer();
 #endif
       mbar_wait(full(s), ph);
 #ifdef FLUTE_DIAGNOSTICS
-      if (first_stage && threadIdx.x == 0) FLUTE_STAMP(3);
-      if (trace) trace[1] = gtimer();
+      if (trace && stage_no < 64) trace[stage_no * 3 + 1] = gtimer();
 #endif
-      first_stage = false;
-
-      // ---- stage -> registers (all loads first), then dequant + MMA ----
-      // NS = sub-units in this stage; full stages (the common case) take the
-      // NS = UPS instantiation, free of per-sub-unit predicates.
-      // this lane's bytes within a sub-unit: W4 16 B at slot*16; W2 8 B at
-      // slot*8; W3 8 B (2-bit plane) at slot*8 + 4 B (1-bit plane) at 2048+slot*4
-      const int slot = kstep * 32 + lane;
-      const uint32_t wst = ws + s * C::kWBytes + slot * (BITS == 4 ? 16 : 8);
-      const uint32_t sst = ss + s * C::kScBytes + (lane >> 2) * 16;
-      const uint32_t xst = xs + s * C::kXBytes;
-      const int glo = (sw.lo_kt * kUnitK) >> gshift;
-      auto run_stage = [&](auto ns_tag) {
-        constexpr int NS = decltype(ns_tag)::value;
-        LaneBits<BITS> lb[NS];
-        uint4 sq[NS];
-        uint32_t bf[NS][MT][2];
+      const uint32_t wst = ws_of(s) + w_lane;
+      const uint32_t sst = ss_of(s) + s_lane;
+      const uint32_t xst = xs_of(s);
+      const int glo = (lo * kUnitK) >> gshift;
+      LaneBits<BITS> lb[NS][KS];
+      uint4 sq[NS];
+      uint32_t bf[NS][KS][MT][2];
 #pragma unroll
-        for (int r = 0; r < NS; ++r) {
-          const uint32_t wr = wst + r * C::kSubBytes;
+      for (int r = 0; r < NS; ++r) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint32_t wr = wst + r * C::kSubBytes + ks * kSlotStride;
           if constexpr (BITS == 4) {
-            lb[r].w = lds128(wr);
+            lb[r][ks].w = lds128(wr);
           } else if constexpr (BITS == 2) {
-            lb[r].w = lds64(wr);
+            lb[r][ks].w = lds64(wr);
           } else {
-            lb[r].hi = lds64(wr);
-            lb[r].lo = lds32(wr - slot * 8 + 2048 + slot * 4);
-          }
-          const int gl = ((((sw.lo_kt + r) << 7) + 16 * kstep) >> gshift) - glo;
-          sq[r] = lds128(sst + gl * 128);
-          if constexpr (MT == 1) {
-            ldsm_x2(xst + xoff[r][0], bf[r][0][0], bf[r][0][1]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < MT / 2; ++q)
-              ldsm_x4(xst + xoff[r][q], bf[r][2 * q][0], bf[r][2 * q][1], bf[r][2 * q + 1][0],
-                      bf[r][2 * q + 1][1]);
+            lb[r][ks].hi = lds64(wr);
+            lb[r][ks].lo = lds32(ws_of(s) + r * C::kSubBytes + 2048 + (slot0 + 32 * ks) * 4);
           }
         }
-        mbar_arrive(empty(s));  // each thread, after its own smem reads
-        if (FLUTE_DIAG(1)) return;
+        // both k-steps (32 k) share one group (group >= 32)
+        const int gl = ((((lo + r) << 7) + kw) >> gshift) - glo;
+        sq[r] = lds128(sst + gl * 128);
+        if constexpr (MT == 1) {
+          ldsm_x4(xst + xoff[r][0], bf[r][0][0][0], bf[r][0][0][1], bf[r][1][0][0], bf[r][1][0][1]);
+        } else {
 #pragma unroll
-        for (int r = 0; r < NS; ++r) {
+          for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+            for (int qq = 0; qq < MT / 2; ++qq)
+              ldsm_x4(xst + xoff[r][ks * (MT / 2) + qq], bf[r][ks][2 * qq][0], bf[r][ks][2 * qq][1],
+                      bf[r][ks][2 * qq + 1][0], bf[r][ks][2 * qq + 1][1]);
+        }
+      }
+      // One arrive per warp: lane 0's release covers the warp's loads (same
+      // instructions, all lanes).
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(s));
+      if (FLUTE_DIAG(1)) return;
+#pragma unroll
+      for (int r = 0; r < NS; ++r) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t scw = j == 0 ? sq[r].x : j == 1 ? sq[r].y : j == 2 ? sq[r].z : sq[r].w;
             uint32_t a[4];
-            lut_dequant4(atom_index_bytes<BITS>(lb[r], j), lane4, lut, scw, a);
+            lut_dequant4(atom_index_bytes<BITS>(lb[r][ks], j), lane4, lut, scw, a);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt) mma_16816(acc[mt][j], a, bf[r][mt][0], bf[r][mt][1]);
-          }
-        }
-      };
-      if (sw.nsub == UPS) {
-        run_stage(std::integral_constant<int, UPS>{});
-      } else if (sw.nsub == 1) {
-        run_stage(std::integral_constant<int, 1>{});
-      } else if constexpr (UPS > 2) {
-        if (sw.nsub == 2) {
-          run_stage(std::integral_constant<int, 2>{});
-        } else if constexpr (UPS > 3) {
-          if (sw.nsub == 3) {
-            run_stage(std::integral_constant<int, 3>{});
-          } else if constexpr (UPS > 4) {
-            // UPS = 8: 4..7 sub-units
-            if (sw.nsub == 4) run_stage(std::integral_constant<int, 4>{});
-            else if (sw.nsub == 5) run_stage(std::integral_constant<int, 5>{});
-            else if (sw.nsub == 6) run_stage(std::integral_constant<int, 6>{});
-            else run_stage(std::integral_constant<int, (UPS > 7 ? 7 : 1)>{});
+            for (int mt = 0; mt < MT; ++mt)
+              mma_16816(acc[mt][j], a, bf[r][ks][mt][0], bf[r][ks][mt][1]);
           }
         }
       }
 #ifdef FLUTE_DIAGNOSTICS
-      if (trace) {
-        // make the timestamp wait for this warp's MMAs to retire
-        float sink = 0.f;
+      if (trace && stage_no < 64) {
+        float sink = 0.f;  // make the stamp wait for this warp's MMAs to retire
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) sink += acc[mt][0][0] + acc[mt][3][3];
-        trace[2] = gtimer() + (sink == 1.2345e-30f ? 1 : 0);
+        trace[stage_no * 3 + 2] = gtimer() + (sink == 1.2345e-30f ? 1 : 0);
       }
       ++stage_no;
 #endif
-      if (!sw.seg_end(ubeg)) continue;
-      // ---- segment end: park the partial for the epilogue warp ----
+    };
+
+    int seg = 0;
+    int parity = 0;  // global stage counter & 1
+    for (int tile = R.t_hi; uend > ubeg && tile >= R.t_lo; --tile, ++seg) {
+      const int bot = R.bot(tile);
+      int kt = R.top(tile);
+      // full stages, then at most one short stage; this half takes every
+      // other stage of the CTA-wide sequence
+      for (; kt - bot + 1 >= UPS; kt -= UPS) {
+        if (parity == half) run_stage(std::integral_constant<int, UPS>{}, kt - UPS + 1, ring.s, ring.ph);
+        ring.advance(S);
+        parity ^= 1;
+      }
+      if constexpr (UPS > 1) {
+        const int rem = kt - bot + 1;
+        if (rem > 0) {
+          if (parity == half) {
+            if (rem == 1) {
+              run_stage(std::integral_constant<int, 1>{}, bot, ring.s, ring.ph);
+            } else if constexpr (UPS > 2) {
+              if (rem == 2) {
+                run_stage(std::integral_constant<int, 2>{}, bot, ring.s, ring.ph);
+              } else if constexpr (UPS > 3) {
+                if (rem == 3) run_stage(std::integral_constant<int, 3>{}, bot, ring.s, ring.ph);
+              }
+            }
+          }
+          ring.advance(S);
+          parity ^= 1;
+        }
+      }
+      // ---- segment end: every warp parks its partial for the epilogue ----
       if (seg > 0) mbar_wait(epi_empty, (seg - 1) & 1);
       const float* accf = &acc[0][0][0];
+      // this warp's rows are all in the vLUT gaps or all in the separate buffer
+      const bool in_lut = warp * C::kFrag < C::kPartRowsInLut;
+      const uint32_t row0 = (in_lut ? lut + warp * C::kFrag * kLutRowBytes + kLutRowBytes / 2
+                                    : part + (warp * C::kFrag - C::kPartRowsInLut) * 128) +
+                            lane * 4u;
+      const uint32_t rstride = in_lut ? kLutRowBytes : 128u;
 #pragma unroll
       for (int i = 0; i < C::kFrag; ++i)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(part + ((warp * C::kFrag + i) * 32 + lane) * 4u),
-                     "f"(accf[i]));
-      mbar_arrive(epi_full);
-      ++seg;
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(row0 + i * rstride), "f"(accf[i]));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(epi_full);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[mt][j][r] = 0.f;
     }
   }
 

@@ -127,34 +127,71 @@ unsigned long long* debug_times_buffer(int workers) {
 
 int bm_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : 32; }
 
-template <int BITS, int BM, int UPS>
-int stages_for() {
-  const size_t cap = props().smem_optin;
-  int s = kMaxStages;
-  while (s > 2 && Cfg<BITS, BM, UPS>::smem_bytes(s) > cap) --s;
-  return s;
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Shared memory available to one CTA when `occ` CTAs must fit on an SM.
+size_t smem_cap(int occ) {
+  static thread_local int dev_cached = -1;
+  static thread_local size_t per_sm = 0, reserved = 0, optin = 0;
+  int dev = 0;
+  FLUTE_CUDA(cudaGetDevice(&dev));
+  if (dev != dev_cached) {
+    int v = 0;
+    FLUTE_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    per_sm = static_cast<size_t>(v);
+    FLUTE_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    reserved = static_cast<size_t>(v);
+    optin = props().smem_optin;
+    dev_cached = dev;
+  }
+  return std::min(optin, per_sm / static_cast<size_t>(occ) - reserved);
 }
 
-// Sub-units per stage (stage depth 128*UPS in k): 8 for m <= 8, 4 for m <= 16,
-// 2 for m <= 32 where a stage's X slice is 4x larger (smem-limited).
-template <int BM>
-constexpr int ups_for() {
-  return BM == 8 ? 8 : BM == 16 ? 4 : 2;
+struct SmemPlan {
+  uint32_t part_off = 0, part_stride = 0, stage_off = 0, stage_bytes = 0, x_bytes = 0, bar_off = 0;
+  uint32_t recv_off = 0;
+  int stages = 0;
+  size_t total = 0;
+};
+
+// [vLUT (+ partial rows in its row gaps) | partials | barriers | stages...],
+// stage = [X (1024-aligned, zero row last) | weights | scales].
+template <int BITS, int BM, int UPS>
+SmemPlan plan_smem(int m, int group, int cluster, size_t cap) {
+  using Cf = Cfg<BITS, BM, UPS>;
+  SmemPlan pl;
+  size_t off = Cf::kLutBytes;
+  pl.part_off = static_cast<uint32_t>(off);
+  pl.part_stride = 128;
+  off += Cf::kPartBytes;
+  pl.recv_off = static_cast<uint32_t>(off);  // cluster split-K receive buffer
+  if (cluster > 1) off += static_cast<size_t>(cluster - 1) * Cf::kFrag * 128;
+  pl.bar_off = static_cast<uint32_t>(off);
+  off = align_up(off + Cf::kBarBytes, 1024);
+  pl.stage_off = static_cast<uint32_t>(off);
+  pl.x_bytes = static_cast<uint32_t>(align_up(2 * UPS * m * 128 + (m < BM ? 128 : 0), 1024));
+  const int ng = UPS * std::max(1, kUnitK / group);
+  pl.stage_bytes =
+      static_cast<uint32_t>(align_up(pl.x_bytes + Cf::kWBytes + static_cast<size_t>(ng) * 128, 1024));
+  const long fit = cap > off ? static_cast<long>((cap - off) / pl.stage_bytes) : 0;
+  pl.stages = static_cast<int>(std::min<long>(kMaxStages, fit));
+  pl.total = off + static_cast<size_t>(pl.stages) * pl.stage_bytes;
+  return pl;
 }
 
-template <int BITS, int BM, int UPS>
+template <int BITS, int BM, int UPS, int OCC>
 void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
-                 long long units, int tiles_k, int gp) {
+                 long long units, int tiles_k, int gp, int cluster) {
   using Cf = Cfg<BITS, BM, UPS>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   FLUTE_CUDA(cudaGetDevice(&dev));
-  const int S = stages_for<BITS, BM, UPS>();
-  const size_t smem = Cf::smem_bytes(S);
+  const SmemPlan pl = plan_smem<BITS, BM, UPS>(m_rows, a.group, cluster, smem_cap(OCC));
+  if (pl.stages < 2) throw flutesim::InternalError("qgemm: shared-memory plan has < 2 stages");
+  auto kern = qgemm_mma_kernel<BITS, BM, UPS, OCC>;
   if (configured_dev != dev) {
-    FLUTE_CUDA(cudaFuncSetAttribute(qgemm_mma_kernel<BITS, BM, UPS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
+    FLUTE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem_cap(OCC))));
     configured_dev = dev;
   }
   const bool x3d = a.k % 64 == 0 && std::getenv("FLUTE_X2D") == nullptr;
@@ -175,51 +212,79 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
   kp.gp = gp;
   kp.units = static_cast<int>(units);
   kp.workers = workers;
-  kp.stages = S;
-  kp.use_ticket = workers > props().sms ? 1 : 0;
+  kp.stages = pl.stages;
+  kp.use_ticket = cluster <= 1 && workers > props().sms * OCC ? 1 : 0;
+  kp.cluster = cluster;
+  kp.recv_off = pl.recv_off;
   kp.x3d = x3d ? 1 : 0;
+  kp.part_off = pl.part_off;
+  kp.part_stride = pl.part_stride;
+  kp.stage_off = pl.stage_off;
+  kp.stage_bytes = pl.stage_bytes;
+  kp.x_bytes = pl.x_bytes;
+  kp.bar_off = pl.bar_off;
   {
     static const char* d = std::getenv("FLUTE_DIAG");
     kp.diag = d ? std::atoi(d) : 0;
   }
   kp.dbg = debug_times_buffer(workers);
+  (void)Cf::kWBytes;
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(workers));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = pl.total;
   cfg.stream = static_cast<cudaStream_t>(a.stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   static const bool no_pdl = std::getenv("FLUTE_NO_PDL") != nullptr;
-  cfg.numAttrs = no_pdl ? 0 : 1;
-  FLUTE_CUDA(cudaLaunchKernelEx(&cfg, qgemm_mma_kernel<BITS, BM, UPS>, map, kp));
+  if (!no_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = static_cast<unsigned>(cluster);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  FLUTE_CUDA(cudaLaunchKernelEx(&cfg, kern, map, kp));
 }
 
+// Per row-block: (stage depth UPS units, CTAs per SM the kernel is built for).
+//   m <= 8 : UPS 2, OCC 2  (co-resident with the next launch)
+//   m <= 16: UPS 1, OCC 2
+//   m <= 32: UPS 2, OCC 1  (64 accumulator floats / lane: one CTA per SM)
 template <int BITS>
 void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
-                 long long units, int tiles_k, int gp) {
+                 long long units, int tiles_k, int gp, int cluster) {
   switch (bm_for(m_rows)) {
-    case 8: {
-#ifdef FLUTE_VARIANTS
-      // Tuning sweep (make diag): FLUTE_VARIANT = sub-units per stage.
-      static const char* v = std::getenv("FLUTE_VARIANT");
-      const std::string vs = v ? v : "";
-      if (vs == "2") return launch_impl<BITS, 8, 2>(a, m_rows, x, y, workers, units, tiles_k, gp);
-      if (vs == "4") return launch_impl<BITS, 8, 4>(a, m_rows, x, y, workers, units, tiles_k, gp);
-#endif
-      launch_impl<BITS, 8, ups_for<8>()>(a, m_rows, x, y, workers, units, tiles_k, gp);
-      break;
-    }
-    case 16:
-      launch_impl<BITS, 16, ups_for<16>()>(a, m_rows, x, y, workers, units, tiles_k, gp);
-      break;
-    default:
-      launch_impl<BITS, 32, ups_for<32>()>(a, m_rows, x, y, workers, units, tiles_k, gp);
-      break;
+    case 8: launch_impl<BITS, 8, 2, 2>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+    case 16: launch_impl<BITS, 16, 1, 2>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+    default: launch_impl<BITS, 32, 2, 1>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
   }
+}
+
+// Cluster split-K (one cluster of C CTAs per 64-column tile, k split C ways,
+// DSMEM reduction) when the tile count T fills >= 3/4 of the SMs with
+// T*C <= #SMs; returns C (1 = no split), or 0 for Stream-K.
+int cluster_for(long long tiles_n, int tiles_k) {
+  if (std::getenv("FLUTE_NO_CLUSTER")) return 0;
+  if (const char* f = std::getenv("FLUTE_FORCE_CLUSTER")) {  // tests: force cluster size C
+    const int c = std::atoi(f);
+    if (c >= 1 && c <= 8 && c <= tiles_k) return c;
+  }
+  const int sms = props().sms;
+  for (int c = 8; c >= 1; c /= 2) {
+    if (c > tiles_k) continue;
+    const long long g = tiles_n * c;
+    if (g <= sms && 4 * g >= 3LL * sms) return c;
+  }
+  return 0;
 }
 
 }  // namespace
@@ -244,9 +309,11 @@ int max_workers(int m) {
 int default_workers(int m, int k, int n, int bits) {
   (void)m;
   (void)bits;
-  const long long units =
-      static_cast<long long>((k + kUnitK - 1) / kUnitK) * ((n + kUnitN - 1) / kUnitN);
-  return static_cast<int>(std::min<long long>(units, props().sms));
+  const int tiles_k = (k + kUnitK - 1) / kUnitK;
+  const long long tiles_n = (n + kUnitN - 1) / kUnitN;
+  const int c = cluster_for(tiles_n, tiles_k);
+  if (c > 0) return static_cast<int>(tiles_n * c);
+  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, props().sms));
 }
 
 void debug_times(unsigned long long* out, int workers) {
@@ -274,10 +341,14 @@ void qgemm(const GemmArgs& a) {
   if (kp % a.group != 0) throw flutesim::ConfigError("qgemm: padded k not divisible by group");
   const int tiles_k = kp / kUnitK;
   const long long units = static_cast<long long>(tiles_k) * (np / kUnitN);
-  int workers = a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits);
+  // default: cluster split-K when the tile count suits it, else Stream-K over
+  // min(units, #SMs) CTAs; an explicit worker count always means Stream-K
+  int cluster = a.workers > 0 ? 0 : cluster_for(np / kUnitN, tiles_k);
+  int workers = cluster > 0 ? static_cast<int>(np / kUnitN) * cluster
+                            : (a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits));
   if (units * (static_cast<long long>(workers) + 1) >= (1LL << 31))
     throw flutesim::ConfigError("qgemm: units x workers exceeds the 32-bit Stream-K index range");
-  if (a.workspace_bytes < workspace_bytes(a.m, workers))
+  if (cluster == 0 && a.workspace_bytes < workspace_bytes(a.m, workers))
     throw flutesim::InputError("qgemm: workspace too small");
   const int gp = kp / a.group;
   // M > 32: 32-row chunks, stream-ordered on one workspace.
@@ -286,9 +357,9 @@ void qgemm(const GemmArgs& a) {
     const void* x = static_cast<const uint8_t*>(a.x) + static_cast<size_t>(r0) * a.k * 2;
     void* y = static_cast<uint8_t*>(a.y) + static_cast<size_t>(r0) * a.n * 2;
     switch (a.bits) {
-      case 2: launch_bits<2>(a, rows, x, y, workers, units, tiles_k, gp); break;
-      case 3: launch_bits<3>(a, rows, x, y, workers, units, tiles_k, gp); break;
-      default: launch_bits<4>(a, rows, x, y, workers, units, tiles_k, gp); break;
+      case 2: launch_bits<2>(a, rows, x, y, workers, units, tiles_k, gp, cluster); break;
+      case 3: launch_bits<3>(a, rows, x, y, workers, units, tiles_k, gp, cluster); break;
+      default: launch_bits<4>(a, rows, x, y, workers, units, tiles_k, gp, cluster); break;
     }
   }
 }

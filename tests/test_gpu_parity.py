@@ -240,3 +240,22 @@ def test_qgemm_baseline_shapes(F, orc, gpu, m, k, n, bits, group):
     y1 = y16.view(np.float16).astype(np.float64)
     normal = np.abs(y1) >= 2.0 ** -14   # f16 subnormal outputs round on a fixed grid
     assert np.array_equal(y2[normal], 2 * y1[normal])
+
+
+@pytest.mark.parametrize("m,k,n,bits,group,cluster", [
+    (1, 512, 256, 4, 128, 2), (5, 1024, 128, 3, 64, 4), (16, 1024, 192, 4, 32, 8),
+    (32, 768, 128, 2, 256, 2), (3, 256, 64, 3, 128, 2), (9, 2048, 64, 4, 128, 1)])
+def test_qgemm_cluster_splitk(F, orc, gpu, monkeypatch, m, k, n, bits, group, cluster):
+    """Cluster split-K mode (one cluster per 64-column tile, DSMEM reduction),
+    forced on small shapes; same bound as the Stream-K path, and bitwise
+    reproducible run to run."""
+    monkeypatch.setenv("FLUTE_FORCE_CLUSTER", str(cluster))
+    rng = np.random.default_rng(77 + m + k + n + bits + cluster)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, emax, ratio = _within(y16, y64)
+    assert ok, f"max err {emax:.4g} ({ratio:.2f} of bound)"
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    again = dw.gemm(x).cpu().numpy().view(np.uint16)
+    assert np.array_equal(again, y16)

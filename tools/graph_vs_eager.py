@@ -14,9 +14,10 @@ dws = [F.DeviceWeights(idx, sc, F.build_nf_table(bits), bits, group) for _ in ra
 x = torch.randn(m, k, dtype=torch.float16, device="cuda")
 y = torch.empty(m, n, dtype=torch.float16, device="cuda")
 st = torch.cuda.Stream()
+W = int(os.environ.get("WORKERS", "0"))
 def run(n_launch):
     for i in range(n_launch):
-        dws[i % R].gemm(x, y, stream=st.cuda_stream)
+        dws[i % R].gemm(x, y, workers=W, stream=st.cuda_stream)
 with torch.cuda.stream(st):
     run(2 * R)
 st.synchronize()
@@ -34,5 +35,5 @@ with torch.cuda.graph(g, stream=st):
 g.replay(); st.synchronize()
 graph = timeit(lambda: [g.replay() for _ in range(5)], 5 * L)
 b = F.algorithmic_bytes(m, k, n, bits, group)
-print(f"M={m} K={k} N={n} W{bits}g{group} R={R} pdl={'off' if os.environ.get('FLUTE_NO_PDL') else 'on'}: "
+print(f"M={m} K={k} N={n} W{bits}g{group} R={R} workers={W or 'default'} pdl={'off' if os.environ.get('FLUTE_NO_PDL') else 'on'}: "
       f"eager {eager:.2f} us ({b/eager/1e3:.0f} GB/s)  graph {graph:.2f} us ({b/graph/1e3:.0f} GB/s)")
