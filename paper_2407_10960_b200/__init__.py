@@ -396,11 +396,19 @@ class DeviceWeights:
                                _stream_ptr(stream)))
         return y
 
-    def gemm_host(self, x16: np.ndarray, workers: int = 0, stream=None) -> np.ndarray:
-        """End-to-end: host f16 bits in, host f16 bits out (copies inside)."""
+    def gemm_host(self, x16: np.ndarray, workers: int = 0, stream=None,
+                  out: Optional[np.ndarray] = None) -> np.ndarray:
+        """End-to-end: host f16 bits in, host f16 bits out (H2D, GEMM, D2H and a
+        stream sync inside).  Pass page-locked arrays (e.g. numpy views of
+        pinned torch tensors) for x16/out to make the copies asynchronous DMA."""
         x16 = np.ascontiguousarray(x16, np.uint16)
         m = x16.shape[0]
-        y = np.zeros((m, self.n), np.uint16)
+        if out is None:
+            y = np.zeros((m, self.n), np.uint16)
+        else:
+            if out.dtype != np.uint16 or out.shape != (m, self.n) or not out.flags.c_contiguous:
+                raise InputError(f"out must be a C-contiguous uint16 [{m}][{self.n}] array")
+            y = out
         _check(_lib.flute_gemm_host(self._h, x16, m, y, workers,
                                     None if stream is None else int(stream)))
         return y

@@ -272,13 +272,18 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 // Cluster split-K (one cluster of C CTAs per 64-column tile, k split C ways,
 // DSMEM reduction) when the tile count T fills >= 3/4 of the SMs with
 // T*C <= #SMs; returns C (1 = no split), or 0 for Stream-K.
-int cluster_for(long long tiles_n, int tiles_k) {
+// CTAs per SM the kernel for an m-row launch is built for (launch_bits).
+int occ_for(int m) { return bm_for(std::min(m, 32)) <= 16 ? 2 : 1; }
+
+int cluster_for(long long tiles_n, int tiles_k, int m) {
   if (std::getenv("FLUTE_NO_CLUSTER")) return 0;
   if (const char* f = std::getenv("FLUTE_FORCE_CLUSTER")) {  // tests: force cluster size C
     const int c = std::atoi(f);
     if (c >= 1 && c <= 8 && c <= tiles_k) return c;
   }
-  const int sms = props().sms;
+  // capacity: all co-resident CTA slots (two per SM for the OCC = 2 kernels,
+  // measured faster than leaving the second slot to the next launch)
+  const int sms = props().sms * occ_for(m);
   for (int c = 8; c >= 1; c /= 2) {
     if (c > tiles_k) continue;
     const long long g = tiles_n * c;
@@ -302,8 +307,7 @@ int sm_count(int device) {
 }
 
 int max_workers(int m) {
-  (void)m;
-  return props().sms;  // one CTA per SM (smem-bound occupancy of 1)
+  return props().sms * occ_for(m);  // co-resident CTA slots
 }
 
 int default_workers(int m, int k, int n, int bits) {
@@ -311,9 +315,9 @@ int default_workers(int m, int k, int n, int bits) {
   (void)bits;
   const int tiles_k = (k + kUnitK - 1) / kUnitK;
   const long long tiles_n = (n + kUnitN - 1) / kUnitN;
-  const int c = cluster_for(tiles_n, tiles_k);
+  const int c = cluster_for(tiles_n, tiles_k, m);
   if (c > 0) return static_cast<int>(tiles_n * c);
-  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, props().sms));
+  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, max_workers(m)));
 }
 
 void debug_times(unsigned long long* out, int workers) {
@@ -343,7 +347,7 @@ void qgemm(const GemmArgs& a) {
   const long long units = static_cast<long long>(tiles_k) * (np / kUnitN);
   // default: cluster split-K when the tile count suits it, else Stream-K over
   // min(units, #SMs) CTAs; an explicit worker count always means Stream-K
-  int cluster = a.workers > 0 ? 0 : cluster_for(np / kUnitN, tiles_k);
+  int cluster = a.workers > 0 ? 0 : cluster_for(np / kUnitN, tiles_k, a.m);
   int workers = cluster > 0 ? static_cast<int>(np / kUnitN) * cluster
                             : (a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits));
   if (units * (static_cast<long long>(workers) + 1) >= (1LL << 31))
