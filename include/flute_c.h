@@ -124,6 +124,25 @@ int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int work
 int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
                     int workers, void* stream);
 
+/* ---- N-column sharding ---------------------------------
+ * Rank `rank` of `world` owns the 64-column tiles [rank*T/world,
+ * (rank+1)*T/world) of T = ceil(n/64): columns [n0, n1).  Its device-layout
+ * weights / scales are the contiguous byte ranges [w_off, w_off+w_bytes) /
+ * [s_off, s_off+s_bytes) of the full buffers (any output may be NULL). */
+int flute_shard_range(int k, int n, int bits, int group, int world, int rank, int* n0, int* n1,
+                      size_t* w_off, size_t* w_bytes, size_t* s_off, size_t* s_bytes);
+/* The all-gather fused into the epilogue: like flute_qgemm, but every output
+ * value is stored to each of y_peers[0..n_peers) (device pointers reachable
+ * from this GPU: NVLink peer or multicast mappings; n_peers <= 8) at
+ * [row * ldy + ycol0 + col].  A rank passes its column offset n0 as ycol0 and
+ * the full N as ldy; after a cross-rank barrier every rank holds the full Y. */
+int flute_qgemm_peers(const void* x, int m, int k, int n, const void* w, const void* scales,
+                      const void* vlut, int bits, int group, void* const* y_peers, int n_peers,
+                      int ldy, int ycol0, void* workspace, size_t workspace_bytes, int workers,
+                      void* stream);
+int flute_gemm_peers(flute_weights* w, const void* x_dev, int m, void* const* y_peers, int n_peers,
+                     int ldy, int ycol0, int workers, void* stream);
+
 /* The reference call itself: flutesim::execute (engine.hpp:72, engine.cpp:345)
  * on HOST buffers in the reference's canonical formats — x f16 [m][k],
  * canonical slices from reorder_and_split at `layout`, scales f16 [n][k/g],

@@ -85,6 +85,20 @@ struct ProblemShape {
 TrafficStats plan_traffic(const ProblemShape& shape);
 
 // ---------------------------------------------------------------------------
+// N-column sharding: rank r of `world` owns the 64-column
+// tiles [r*T/world, (r+1)*T/world) of the T = ceil(n/64) tiles, i.e. columns
+// [n0, n1).  Because device-layout units are n-tile major, the shard's packed
+// weights and scales are one contiguous byte range of the full device buffers.
+// ---------------------------------------------------------------------------
+
+struct ShardRange {
+  int n0 = 0, n1 = 0;                  // columns
+  std::size_t w_off = 0, w_bytes = 0;  // into the full device-layout weights
+  std::size_t s_off = 0, s_bytes = 0;  // into the full device-layout scales
+};
+ShardRange shard_range(int k, int n, int bits, int group, int world, int rank);
+
+// ---------------------------------------------------------------------------
 // Device-resident path (new): upload once, call many times.
 // ---------------------------------------------------------------------------
 
@@ -104,6 +118,12 @@ class DeviceWeights {
   int n() const;
   // y_dev[m][n] = x_dev[m][k] * W_hat, device pointers, async on `stream`.
   void gemm(const Half* x_dev, int m, Half* y_dev, int workers = 0, void* stream = nullptr);
+  // N-sharded layer: store this GEMM's [m][n] result into every y_peers[i]
+  // (device pointers reachable from this GPU — NVLink peer or multicast
+  // mappings) at [row * ldy + ycol0 + col]: the all-gather fused into the
+  // epilogue.  The caller synchronises ranks before reading the full Y.
+  void gemm_peers(const Half* x_dev, int m, void* const* y_peers, int n_peers, int ldy, int ycol0,
+                  int workers = 0, void* stream = nullptr);
   // Host in / host out (copies inside; synchronizes the stream).
   MatH gemm_host(const MatH& x, int workers = 0, void* stream = nullptr);
   // Raw host buffers (f16 bits; pinned memory makes the copies truly async).

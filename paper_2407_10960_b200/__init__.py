@@ -123,6 +123,15 @@ _SIGS = {
     "flute_execute": (C.c_int, [_u16p, C.c_int, _u32p, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                 _i32p, _u16p, _u32p, C.c_int, C.c_int, C.c_int, C.c_int, _u16p,
                                 _u64p]),
+    "flute_shard_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                    C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "flute_qgemm_peers": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int,
+                                    C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
+                                    _vp, C.c_size_t, C.c_int, _vp]),
+    "flute_gemm_peers": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                   C.c_int, C.c_int, _vp]),
     "flute_dequant_all_device": (C.c_int, [_u32p, C.c_int, _u16p, C.c_int, _u32p]),
     "flute_mma_fragment": (C.c_int, [_u16p, _u16p, _f32p, C.c_int, C.c_int, C.c_int]),
     "flute_debug_times": (C.c_int, [_u64p, C.c_int]),
@@ -396,6 +405,19 @@ class DeviceWeights:
                                _stream_ptr(stream)))
         return y
 
+    def gemm_peers(self, x, y_ptrs: Sequence[int], ldy: int, ycol0: int, workers: int = 0,
+                   stream=None) -> None:
+        """Store this GEMM's [m][n] result into every device buffer in y_ptrs
+        (row stride ldy, column offset ycol0): the N-sharded all-gather fused
+        into the epilogue (flute_gemm_peers)."""
+        import torch
+        if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
+            raise InputError(f"x must be a cuda float16 [m][{self.k}] tensor")
+        x = x.contiguous()
+        arr = (C.c_void_p * len(y_ptrs))(*[int(p) for p in y_ptrs])
+        _check(_lib.flute_gemm_peers(self._h, x.data_ptr(), x.shape[0], arr, len(y_ptrs), ldy,
+                                     ycol0, workers, _stream_ptr(stream)))
+
     def gemm_host(self, x16: np.ndarray, workers: int = 0, stream=None,
                   out: Optional[np.ndarray] = None) -> np.ndarray:
         """End-to-end: host f16 bits in, host f16 bits out (H2D, GEMM, D2H and a
@@ -452,6 +474,25 @@ def execute(x16: np.ndarray, slices, k: int, n: int, bits: int, group: int, scal
                               np.ascontiguousarray(vlut_words, np.uint32), dup, workers, stages,
                               tile_m, y, st))
     return MatmulResult(y, dict(zip(TRAFFIC_FIELDS, (int(v) for v in st))))
+
+
+@dataclass
+class ShardRange:
+    n0: int
+    n1: int
+    w_off: int
+    w_bytes: int
+    s_off: int
+    s_bytes: int
+
+
+def shard_range(k: int, n: int, bits: int, group: int, world: int, rank: int) -> ShardRange:
+    """Columns and device-layout byte ranges owned by `rank` (flute_shard_range)."""
+    n0, n1 = C.c_int(0), C.c_int(0)
+    v = [C.c_size_t(0) for _ in range(4)]
+    _check(_lib.flute_shard_range(k, n, bits, group, world, rank, C.byref(n0), C.byref(n1),
+                                  *[C.byref(x) for x in v]))
+    return ShardRange(n0.value, n1.value, *[x.value for x in v])
 
 
 def dequant_all_device(vlut_words: np.ndarray, bits: int, scales: np.ndarray) -> np.ndarray:

@@ -483,6 +483,56 @@ int flute_execute(const uint16_t* x, int m, const uint32_t* slice_hi, const uint
   });
 }
 
+int flute_shard_range(int k, int n, int bits, int group, int world, int rank, int* n0, int* n1,
+                      size_t* w_off, size_t* w_bytes, size_t* s_off, size_t* s_bytes) {
+  return guard([&] {
+    const ShardRange r = shard_range(k, n, bits, group, world, rank);
+    if (n0) *n0 = r.n0;
+    if (n1) *n1 = r.n1;
+    if (w_off) *w_off = r.w_off;
+    if (w_bytes) *w_bytes = r.w_bytes;
+    if (s_off) *s_off = r.s_off;
+    if (s_bytes) *s_bytes = r.s_bytes;
+  });
+}
+
+int flute_qgemm_peers(const void* x, int m, int k, int n, const void* w, const void* scales,
+                      const void* vlut, int bits, int group, void* const* y_peers, int n_peers,
+                      int ldy, int ycol0, void* workspace, size_t workspace_bytes, int workers,
+                      void* stream) {
+  return guard([&] {
+    flute_dev::GemmArgs a;
+    a.x = x;
+    a.m = m;
+    a.k = k;
+    a.n = n;
+    a.w = w;
+    a.scales = scales;
+    a.vlut = vlut;
+    a.bits = bits;
+    a.group = group;
+    a.y_peers = y_peers;
+    a.n_peers = n_peers;
+    a.ldy = ldy;
+    a.ycol0 = ycol0;
+    a.workspace = workspace;
+    a.workspace_bytes = workspace_bytes;
+    a.workers = workers;
+    a.stream = stream;
+    if (n_peers < 1) throw ConfigError("qgemm_peers: need at least one output buffer");
+    flute_dev::qgemm(a);
+  });
+}
+
+int flute_gemm_peers(flute_weights* w, const void* x_dev, int m, void* const* y_peers, int n_peers,
+                     int ldy, int ycol0, int workers, void* stream) {
+  return guard([&] {
+    need(w, "weights");
+    w->impl->gemm_peers(static_cast<const Half*>(x_dev), m, y_peers, n_peers, ldy, ycol0, workers,
+                        stream);
+  });
+}
+
 int flute_dequant_all_device(const uint32_t* vlut_words, int bits, const uint16_t* scales,
                              int n_scales, uint32_t* out_host) {
   return guard([&] {

@@ -16,6 +16,12 @@ struct GemmArgs {
   const void* vlut = nullptr;    // 2^(2b) device-order u32 words, device
   int bits = 4, group = 128;
   void* y = nullptr;             // f16 [m][n], device
+  // Fused all-gather (N-sharded layer): when n_peers > 0, Y is stored to every
+  // y_peers[i] (device pointers reachable from this GPU: peer / multicast
+  // mappings) at [row * ldy + ycol0 + col]; y is then ignored.
+  void* const* y_peers = nullptr;
+  int n_peers = 0;
+  int ldy = 0, ycol0 = 0;
   void* workspace = nullptr;
   std::size_t workspace_bytes = 0;
   int workers = 0;               // <= 0: default

@@ -143,7 +143,8 @@ struct DeviceWeights::Impl {
     flute_dev::stream_sync(nullptr);
   }
 
-  void gemm(const void* x, int m, void* y, int workers, void* stream) {
+  void gemm(const void* x, int m, void* y, int workers, void* stream,
+            void* const* y_peers = nullptr, int n_peers = 0, int ldy = 0, int ycol0 = 0) {
     if (workers > 0 && flute_dev::workspace_bytes(m, workers) > ws.bytes) {
       ws = DeviceBuffer(flute_dev::workspace_bytes(m, workers));
       flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
@@ -164,6 +165,10 @@ struct DeviceWeights::Impl {
     a.workspace_bytes = ws.bytes;
     a.workers = workers;
     a.stream = stream;
+    a.y_peers = y_peers;
+    a.n_peers = n_peers;
+    a.ldy = ldy;
+    a.ycol0 = ycol0;
     flute_dev::qgemm(a);
   }
 };
@@ -204,6 +209,12 @@ int DeviceWeights::n() const { return impl_->n; }
 
 void DeviceWeights::gemm(const Half* x_dev, int m, Half* y_dev, int workers, void* stream) {
   impl_->gemm(x_dev, m, y_dev, workers, stream);
+}
+
+void DeviceWeights::gemm_peers(const Half* x_dev, int m, void* const* y_peers, int n_peers,
+                               int ldy, int ycol0, int workers, void* stream) {
+  if (n_peers < 1) throw ConfigError("gemm_peers: need at least one output buffer");
+  impl_->gemm(x_dev, m, nullptr, workers, stream, y_peers, n_peers, ldy, ycol0);
 }
 
 MatH DeviceWeights::gemm_host(const MatH& x, int workers, void* stream) {
@@ -255,6 +266,27 @@ MatmulResult execute(const MatmulProblem& problem) {
   MatmulResult r;
   r.y = dw.gemm_host(*problem.x, problem.workers, nullptr);
   r.stats = account(s, problem.workers);
+  return r;
+}
+
+ShardRange shard_range(int k, int n, int bits, int group, int world, int rank) {
+  if (world < 1 || rank < 0 || rank >= world) {
+    throw ConfigError("shard_range: need world >= 1 and 0 <= rank < world");
+  }
+  const DeviceGeometry g = device_geometry(k, n, bits, group);
+  const int T = g.tiles_n();
+  if (world > T) throw ConfigError("shard_range: more ranks than 64-column tiles");
+  const int t0 = static_cast<int>(static_cast<long>(T) * rank / world);
+  const int t1 = static_cast<int>(static_cast<long>(T) * (rank + 1) / world);
+  ShardRange r;
+  r.n0 = t0 * kUnitN;
+  r.n1 = std::min(t1 * kUnitN, n);
+  const std::size_t tile_w = g.unit_bytes() * static_cast<std::size_t>(g.tiles_k());
+  const std::size_t tile_s = static_cast<std::size_t>(g.groups_padded()) * kUnitN * 2;
+  r.w_off = tile_w * t0;
+  r.w_bytes = tile_w * (t1 - t0);
+  r.s_off = tile_s * t0;
+  r.s_bytes = tile_s * (t1 - t0);
   return r;
 }
 

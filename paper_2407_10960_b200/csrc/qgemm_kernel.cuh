@@ -50,11 +50,18 @@ constexpr int kMaxStages = 16;
 constexpr int kUnitN = 64;   // == flutesim::kUnitN (pack.hpp)
 constexpr int kUnitK = 128;  // == flutesim::kUnitK: one Stream-K unit
 
+constexpr int kMaxPeers = 8;
+
 struct KParams {
   const uint8_t* w;
   const uint8_t* sc;
   const uint32_t* vlut;
-  __half* y;
+  // Output: every value is stored to y_out[0..n_out) at [row * ldy + ycol0 + col].
+  // n_out = 1, ldy = n, ycol0 = 0 is the plain GEMM; n_out > 1 with peer
+  // pointers is the N-sharded layer's all-gather fused into the epilogue (each
+  // rank writes its column slice straight into every rank's full Y).
+  __half* y_out[kMaxPeers];
+  int n_out, ldy, ycol0;
   float* slots;
   uint32_t* flags;
   int m, n;
@@ -427,8 +434,11 @@ __global__ void __launch_bounds__(kThreads, OCC)
           for (int r = 0; r < 4; ++r) {
             const int row = mt * 8 + 2 * t + (r & 1);
             const int col = ncol0 + 16 * j + g + 8 * (r >> 1);
-            if (row < p.m && col < p.n)
-              p.y[static_cast<size_t>(row) * p.n + col] = __float2half_rn(accf[(mt * 4 + j) * 4 + r]);
+            if (row < p.m && col < p.n) {
+              const __half v = __float2half_rn(accf[(mt * 4 + j) * 4 + r]);
+              const size_t off = static_cast<size_t>(row) * p.ldy + p.ycol0 + col;
+              for (int d = 0; d < p.n_out; ++d) p.y_out[d][off] = v;
+            }
           }
     }
   } else {

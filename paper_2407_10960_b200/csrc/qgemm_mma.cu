@@ -200,7 +200,21 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
   kp.w = static_cast<const uint8_t*>(a.w);
   kp.sc = static_cast<const uint8_t*>(a.scales);
   kp.vlut = static_cast<const uint32_t*>(a.vlut);
-  kp.y = static_cast<__half*>(y);
+  if (a.n_peers > 0) {
+    // y points at the row-0 slot of this launch's row chunk in peer 0's buffer;
+    // the same row offset applies to every peer
+    const size_t row_off = static_cast<const uint8_t*>(y) - static_cast<const uint8_t*>(a.y_peers[0]);
+    for (int i = 0; i < a.n_peers; ++i)
+      kp.y_out[i] = reinterpret_cast<__half*>(static_cast<uint8_t*>(a.y_peers[i]) + row_off);
+    kp.n_out = a.n_peers;
+    kp.ldy = a.ldy;
+    kp.ycol0 = a.ycol0;
+  } else {
+    kp.y_out[0] = static_cast<__half*>(y);
+    kp.n_out = 1;
+    kp.ldy = a.n;
+    kp.ycol0 = 0;
+  }
   const size_t flag_bytes = (static_cast<size_t>(workers) + 2) * 4;
   const size_t flag_span = (flag_bytes + 255) / 256 * 256;
   kp.flags = static_cast<uint32_t*>(a.workspace);
@@ -338,8 +352,16 @@ void qgemm(const GemmArgs& a) {
   if (a.bits < 2 || a.bits > 4) throw flutesim::ConfigError("qgemm: bits must be 2, 3 or 4");
   if (a.k % 16 != 0 || a.n % 16 != 0 || a.k < 16 || a.n < 16)
     throw flutesim::ConfigError("qgemm: k and n must be positive multiples of 16");
-  if (!a.x || !a.w || !a.scales || !a.vlut || !a.y || !a.workspace)
+  if (!a.x || !a.w || !a.scales || !a.vlut || !a.workspace || (a.n_peers == 0 && !a.y))
     throw flutesim::InputError("qgemm: null device pointer");
+  if (a.n_peers < 0 || a.n_peers > kMaxPeers)
+    throw flutesim::ConfigError("qgemm: n_peers must be in [0, 8]");
+  if (a.n_peers > 0) {
+    for (int i = 0; i < a.n_peers; ++i)
+      if (!a.y_peers || !a.y_peers[i]) throw flutesim::InputError("qgemm: null peer output pointer");
+    if (a.ycol0 < 0 || a.ldy < a.ycol0 + a.n)
+      throw flutesim::ConfigError("qgemm: peer output needs ldy >= ycol0 + n");
+  }
   const int kp = (a.k + kUnitK - 1) / kUnitK * kUnitK;
   const int np = (a.n + kUnitN - 1) / kUnitN * kUnitN;
   if (kp % a.group != 0) throw flutesim::ConfigError("qgemm: padded k not divisible by group");
@@ -359,7 +381,9 @@ void qgemm(const GemmArgs& a) {
   for (int r0 = 0; r0 < a.m; r0 += 32) {
     const int rows = std::min(32, a.m - r0);
     const void* x = static_cast<const uint8_t*>(a.x) + static_cast<size_t>(r0) * a.k * 2;
-    void* y = static_cast<uint8_t*>(a.y) + static_cast<size_t>(r0) * a.n * 2;
+    void* y = a.n_peers > 0
+                  ? static_cast<void*>(static_cast<uint8_t*>(a.y_peers[0]) + static_cast<size_t>(r0) * a.ldy * 2)
+                  : static_cast<void*>(static_cast<uint8_t*>(a.y) + static_cast<size_t>(r0) * a.n * 2);
     switch (a.bits) {
       case 2: launch_bits<2>(a, rows, x, y, workers, units, tiles_k, gp, cluster); break;
       case 3: launch_bits<3>(a, rows, x, y, workers, units, tiles_k, gp, cluster); break;
