@@ -394,6 +394,75 @@ def run_ours(args):
     return 0
 
 
+def run_sharded_70b(args):
+    """BASELINE.json configs[3]: one LLaMA-3-70B MLP layer (K=8192, N=28672, W4
+    NF g128, M=1), N-sharded over the ranks; a step = each rank's shard GEMM +
+    the output all-gather (NCCL, or the fused peer-store epilogue with
+    --allgather peer).  Strong scaling: the layer is fixed as N grows."""
+    import torch
+    import torch.distributed as dist
+    import paper_2407_10960_b200 as F
+    from paper_2407_10960_b200.sharded import ShardedWeights
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local))
+    k, n, bits, group, m = 8192, 28672, 4, 128, 1
+    rng = np.random.default_rng(70)
+    w = rng.standard_normal((k, n), dtype=np.float32)
+    idx, scales = F.quantize_matrix(w, bits, group)
+    table = F.build_nf_table(bits)
+    shard_bytes = F.shard_range(k, n, bits, group, world, rank).w_bytes
+    reps = max(2, int(np.ceil(3 * 126e6 / shard_bytes)))
+    sws = [ShardedWeights(idx, scales, table, bits, group, rank, world, mode=args.allgather)
+           for _ in range(min(reps, 24))]
+    x = torch.from_numpy((rng.standard_normal((m, k)) * 0.5).astype(np.float16)).cuda()
+    layer_bytes = algo_bytes(m, k, n, bits, group)
+    for i in range(args.warmup):
+        sws[i % len(sws)].gemm(x)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        y = sws[i % len(sws)].gemm(x)
+    e1.record()
+    e1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    peak, peak_kind = peaks()
+    if rank == 0:
+        per_gpu = (shard_bytes + F.shard_range(k, n, bits, group, world, 0).s_bytes + m * k * 2
+                   + m * (n // world) * 2) / (ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": METRIC, "value": round(layer_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 6),
+            "us_per_layer": round(ms * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic (N(0,1) weights NF4 g128)",
+            "config": {"workload": "BASELINE configs[3]: LLaMA-3-70B layer K=8192 N=28672 W4 g128 "
+                                   "M=1, N-sharded + output all-gather",
+                       "allgather": args.allgather, "layer_bytes": layer_bytes,
+                       "l2": f"{len(sws)} weight replicas rotated (>= 3x L2 per rank)"},
+            "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_gpu / peak, 4), "peak_kind": peak_kind,
+                         "note": "per-GPU shard bytes / step time (includes the all-gather)"},
+            "gpu_launches": args.steps, "clocks": clocks}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,11 +471,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--quick", action="store_true", help="skip per-case micro-benchmarks")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--workload", default="mlp8b", choices=["mlp8b", "70b"],
+                    help="mlp8b: configs[1] (default, weak scaling); 70b: configs[3] N-sharded")
+    ap.add_argument("--allgather", default="nccl", choices=["nccl", "peer"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.workload == "70b":
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29531", RANK="0", WORLD_SIZE="1",
+                              LOCAL_RANK="0")
+        return run_sharded_70b(args)
     return run_ours(args)
 
 
