@@ -29,6 +29,16 @@ struct GemmArgs {
 };
 
 void qgemm(const GemmArgs& a);
+
+// Compute-bound path (qgemm_tc.cu): tcgen05/TMEM kernel used by qgemm() for
+// m >= 64 (unless FLUTE_NO_TC is set).  Split-K partials live in the caller's
+// workspace; tc_workspace_bytes is the size for the full split count.
+bool tc_enabled(int m);
+std::size_t tc_workspace_bytes(int m, int k, int n, int sms);
+void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, void* part,
+              std::size_t part_bytes);
+// Workspace a qgemm call with these dimensions needs (either path).
+std::size_t call_workspace_bytes(int m, int k, int n, int workers);
 std::size_t workspace_bytes(int m, int workers);
 int max_workers(int m);
 int default_workers(int m, int k, int n, int bits);

@@ -145,8 +145,9 @@ struct DeviceWeights::Impl {
 
   void gemm(const void* x, int m, void* y, int workers, void* stream,
             void* const* y_peers = nullptr, int n_peers = 0, int ldy = 0, int ycol0 = 0) {
-    if (workers > 0 && flute_dev::workspace_bytes(m, workers) > ws.bytes) {
-      ws = DeviceBuffer(flute_dev::workspace_bytes(m, workers));
+    const std::size_t need = flute_dev::call_workspace_bytes(m, k, n, workers);
+    if (need > ws.bytes) {
+      ws = DeviceBuffer(need);
       flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
       flute_dev::stream_sync(nullptr);
     }

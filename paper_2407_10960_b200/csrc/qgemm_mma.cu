@@ -347,6 +347,11 @@ size_t workspace_bytes(int m, int workers) {
   return flag_span + static_cast<size_t>(workers) * (bm / 8) * 16 * 32 * 4;
 }
 
+size_t call_workspace_bytes(int m, int k, int n, int workers) {
+  const size_t mma = workspace_bytes(std::min(m, 32), workers > 0 ? workers : max_workers(std::min(m, 32)) * 4);
+  return tc_enabled(m) ? std::max(mma, tc_workspace_bytes(m, k, n, props().sms)) : mma;
+}
+
 void qgemm(const GemmArgs& a) {
   if (a.m < 1) throw flutesim::ConfigError("qgemm: m must be >= 1");
   if (a.bits < 2 || a.bits > 4) throw flutesim::ConfigError("qgemm: bits must be 2, 3 or 4");
@@ -374,9 +379,15 @@ void qgemm(const GemmArgs& a) {
                             : (a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits));
   if (units * (static_cast<long long>(workers) + 1) >= (1LL << 31))
     throw flutesim::ConfigError("qgemm: units x workers exceeds the 32-bit Stream-K index range");
-  if (cluster == 0 && a.workspace_bytes < workspace_bytes(a.m, workers))
+  if (cluster == 0 && !(a.n_peers == 0 && tc_enabled(a.m)) &&
+      a.workspace_bytes < workspace_bytes(a.m, workers))
     throw flutesim::InputError("qgemm: workspace too small");
   const int gp = kp / a.group;
+  if (a.n_peers == 0 && tc_enabled(a.m)) {
+    // compute-bound regime: one tcgen05 launch over all rows
+    qgemm_tc(a, tiles_k, np / kUnitN, gp, props().sms, a.workspace, a.workspace_bytes);
+    return;
+  }
   // M > 32: 32-row chunks, stream-ordered on one workspace.
   for (int r0 = 0; r0 < a.m; r0 += 32) {
     const int rows = std::min(32, a.m - r0);

@@ -259,3 +259,41 @@ def test_qgemm_cluster_splitk(F, orc, gpu, monkeypatch, m, k, n, bits, group, cl
     x = gpu.from_numpy(x16.view(np.float16)).cuda()
     again = dw.gemm(x).cpu().numpy().view(np.uint16)
     assert np.array_equal(again, y16)
+
+
+TC_CASES = [  # (m, k, n, bits, group, splits) — compute-bound tcgen05 path (m >= 64)
+    (64, 256, 128, 4, 128, 1), (64, 1024, 256, 4, 32, 4), (100, 512, 192, 3, 64, 2),
+    (128, 512, 384, 2, 256, 1), (200, 384, 320, 4, 128, 3), (256, 1024, 128, 3, 128, 0),
+    (512, 2048, 512, 4, 128, 0), (65, 128, 64, 2, 32, 1),
+]
+
+
+@pytest.mark.parametrize("m,k,n,bits,group,splits", TC_CASES)
+def test_qgemm_tcgen05_vs_oracle(F, orc, gpu, monkeypatch, m, k, n, bits, group, splits):
+    """M >= 64 runs the tcgen05/TMEM kernel (UMMA from the dequantised W^T tile
+    in swizzled smem, fp32 accumulator in TMEM, optional split-K): same bound
+    as the memory-bound path, deterministic run to run."""
+    if splits:
+        monkeypatch.setenv("FLUTE_TC_SPLITS", str(splits))
+    rng = np.random.default_rng(5000 + m + k + n + bits + group)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, emax, ratio = _within(y16, y64)
+    assert ok, f"max err {emax:.4g} ({ratio:.2f} of bound)"
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    assert np.array_equal(dw.gemm(x).cpu().numpy().view(np.uint16), y16)
+
+
+def test_qgemm_tcgen05_matches_mma_path(F, orc, gpu, monkeypatch):
+    """The tcgen05 path and the mma.sync path (forced with FLUTE_NO_TC) agree
+    within the parity bound on a BASELINE configs[4]-style shape."""
+    rng = np.random.default_rng(44)
+    m, k, n, bits, group = 256, 4096, 1024, 4, 128
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y_tc, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    monkeypatch.setenv("FLUTE_NO_TC", "1")
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    y_mma = dw.gemm(x).cpu().numpy().view(np.uint16)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    assert _within(y_tc, y64)[0] and _within(y_mma, y64)[0]
