@@ -297,3 +297,19 @@ def test_qgemm_tcgen05_matches_mma_path(F, orc, gpu, monkeypatch):
     y_mma = dw.gemm(x).cpu().numpy().view(np.uint16)
     y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
     assert _within(y_tc, y64)[0] and _within(y_mma, y64)[0]
+
+
+def test_execute_abi_reference_formats(F, orc, gpu):
+    """flute_execute: the reference call (engine.hpp:72) on host buffers in the
+    reference's own formats (canonical slices, dup-2 vLUT) — y within the
+    bound of the reference engine's output, stats == plan_traffic."""
+    rng = np.random.default_rng(31)
+    m, k, n, bits, group = 5, 512, 256, 3, 128
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    slices = F.reorder_and_split(idx, bits)
+    vlut = F.make_vectorized_lut(table, bits, dup=2)
+    res = F.execute(x16, slices, k, n, bits, group, scales, vlut, dup=2, workers=3)
+    yref, _ = orc.execute(x16, orc.pack(idx, bits), k, n, bits, group, scales, table, workers=3)
+    ok, err, _ = _within(res.y, yref.view(np.float16).astype(np.float64))
+    assert ok, err
+    assert res.stats == F.plan_traffic(m, k, n, bits, group, workers=3)
