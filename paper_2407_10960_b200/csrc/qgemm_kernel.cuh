@@ -426,20 +426,23 @@ __global__ void __launch_bounds__(kThreads, OCC)
       // write Y (f16, RNE); accf[(mt*4 + j)*4 + r] is C[n][m] of atom j, m-tile mt
       const int g = lane >> 2, t = lane & 3;
       const int ncol0 = tile * kUnitN;
+      // one copy of the store code per output buffer (the peer loop stays
+      // rolled: unrolling it inside the fragment loops quadruples the kernel)
+#pragma unroll 1
+      for (int d = 0; d < p.n_out; ++d) {
+        __half* yb = p.y_out[d] + p.ycol0;
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 4; ++j)
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int row = mt * 8 + 2 * t + (r & 1);
-            const int col = ncol0 + 16 * j + g + 8 * (r >> 1);
-            if (row < p.m && col < p.n) {
-              const __half v = __float2half_rn(accf[(mt * 4 + j) * 4 + r]);
-              const size_t off = static_cast<size_t>(row) * p.ldy + p.ycol0 + col;
-              for (int d = 0; d < p.n_out; ++d) p.y_out[d][off] = v;
+            for (int r = 0; r < 4; ++r) {
+              const int row = mt * 8 + 2 * t + (r & 1);
+              const int col = ncol0 + 16 * j + g + 8 * (r >> 1);
+              if (row < p.m && col < p.n)
+                yb[static_cast<size_t>(row) * p.ldy + col] = __float2half_rn(accf[(mt * 4 + j) * 4 + r]);
             }
-          }
+      }
     }
   } else {
     // ===================== consumers =====================

@@ -3,7 +3,7 @@
 R weight replicas rotated (R large = cold HBM).  usage: M K N BITS GROUP [R]"""
 import os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("PKGROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2407_10960_b200 as F
 
 m, k, n, bits, group = (int(v) for v in sys.argv[1:6])
