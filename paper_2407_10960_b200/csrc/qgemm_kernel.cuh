@@ -120,6 +120,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // Diagnostics (timeline stamps, FLUTE_DIAG bits) exist only in builds with
 // -DFLUTE_DIAGNOSTICS (make diag); the product build compiles them out.
+#ifndef FLUTE_SLEEP_PRODUCER
+#define FLUTE_SLEEP_PRODUCER 1
+#endif
 #ifdef FLUTE_DIAGNOSTICS
 #define FLUTE_STAMP(slot)                                                     \
   do {                                                                        \
@@ -306,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, OCC)
         for (int kt = R.top(t); kt >= bot; kt -= UPS, ++it) {
           const int lo = kt - UPS + 1 > bot ? kt - UPS + 1 : bot;
           if (it >= pre) {
-            mbar_wait(empty(ring.s), ring.ph ^ 1u);
+            if (FLUTE_SLEEP_PRODUCER) mbar_wait_sleep(empty(ring.s), ring.ph ^ 1u);
+            else mbar_wait(empty(ring.s), ring.ph ^ 1u);
             issue_ws(t, lo, kt - lo + 1, ring.s);
           }
           issue_x(lo, kt - lo + 1, ring.s);
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
     int seg = 0;
     for (int tile = R.t_hi; uend > ubeg && tile >= R.t_lo; --tile, ++seg) {
       // fixed-order sum of the 8 warp partials, then free the buffer
-      mbar_wait(epi_full, seg & 1);
+      mbar_wait_sleep(epi_full, seg & 1);
       float accf[C::kFrag];
 #pragma unroll
       for (int i = 0; i < C::kFrag; ++i) {
