@@ -117,6 +117,9 @@ int flute_weights_from_indices(const uint8_t* indices, const uint16_t* scales,
                                const float* table_values, int k, int n, int bits, int group,
                                flute_weights** out);
 int flute_weights_destroy(flute_weights* w);
+/* Pre-size the handle's device workspace for calls with m <= max_m so that no
+ * later flute_gemm allocates (required before CUDA-graph capture of m > 32). */
+int flute_weights_reserve(flute_weights* w, int max_m);
 int flute_weights_info(const flute_weights* w, int* k, int* n, int* bits, int* group);
 int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int workers,
                void* stream);

@@ -116,6 +116,10 @@ class DeviceWeights {
 
   int k() const;
   int n() const;
+  // Pre-size the device workspace for calls with m <= max_m (default workers),
+  // so no later call allocates (e.g. inside CUDA-graph capture).  Calls with
+  // m <= 32 never allocate; larger m (tcgen05 split-K partials) may on first use.
+  void reserve(int max_m);
   // y_dev[m][n] = x_dev[m][k] * W_hat, device pointers, async on `stream`.
   void gemm(const Half* x_dev, int m, Half* y_dev, int workers = 0, void* stream = nullptr);
   // N-sharded layer: store this GEMM's [m][n] result into every y_peers[i]

@@ -116,6 +116,7 @@ _SIGS = {
     "flute_weights_from_indices": (C.c_int, [_u8p, _u16p, _f32p, C.c_int, C.c_int, C.c_int,
                                              C.c_int, C.POINTER(_vp)]),
     "flute_weights_destroy": (C.c_int, [_vp]),
+    "flute_weights_reserve": (C.c_int, [_vp, C.c_int]),
     "flute_weights_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "flute_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _vp]),
@@ -380,6 +381,11 @@ class DeviceWeights:
                                          group, C.byref(h)))
         self._h = h
         return self
+
+    def reserve(self, max_m: int) -> None:
+        """Pre-size the workspace for m <= max_m (no allocation in later calls,
+        e.g. inside CUDA-graph capture; m <= 32 never allocates)."""
+        _check(_lib.flute_weights_reserve(self._h, max_m))
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -425,6 +425,14 @@ int flute_weights_info(const flute_weights* w, int* k, int* n, int* bits, int* g
   });
 }
 
+int flute_weights_reserve(flute_weights* w, int max_m) {
+  return guard([&] {
+    need(w, "weights");
+    if (max_m < 1) throw ConfigError("reserve: max_m must be >= 1");
+    w->impl->reserve(max_m);
+  });
+}
+
 int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int workers,
                void* stream) {
   return guard([&] {

@@ -137,10 +137,22 @@ struct DeviceWeights::Impl {
     flute_dev::h2d(w.p, packed.data(), packed.size(), nullptr);
     flute_dev::h2d(sc.p, scales.data(), scales.size() * 2, nullptr);
     flute_dev::h2d(lut.p, lut_words.data(), lut_words.size() * 4, nullptr);
-    const int maxw = std::max(flute_dev::max_workers(32), 1) * 4;  // ticket mode headroom
-    ws = DeviceBuffer(flute_dev::workspace_bytes(32, maxw));
-    flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
-    flute_dev::stream_sync(nullptr);
+    // every m <= 32 default-worker call fits without growing (growth is a
+    // synchronous allocation, not allowed inside CUDA-graph capture)
+    reserve(32);
+  }
+
+  // Size the workspace for every call with m <= max_m and default workers.
+  void reserve(int max_m) {
+    std::size_t need = 0;
+    for (int m = 1; m <= max_m; m = m < 32 ? std::min(32, m * 2) : m + 32)
+      need = std::max(need, flute_dev::call_workspace_bytes(m, k, n, 0));
+    need = std::max(need, flute_dev::call_workspace_bytes(max_m, k, n, 0));
+    if (need > ws.bytes) {
+      ws = DeviceBuffer(need);
+      flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
+      flute_dev::stream_sync(nullptr);
+    }
   }
 
   void gemm(const void* x, int m, void* y, int workers, void* stream,
@@ -206,6 +218,7 @@ DeviceWeights::DeviceWeights(const std::vector<std::uint8_t>& indices,
 
 DeviceWeights::~DeviceWeights() = default;
 int DeviceWeights::k() const { return impl_->k; }
+void DeviceWeights::reserve(int max_m) { impl_->reserve(max_m); }
 int DeviceWeights::n() const { return impl_->n; }
 
 void DeviceWeights::gemm(const Half* x_dev, int m, Half* y_dev, int workers, void* stream) {

@@ -313,3 +313,26 @@ def test_execute_abi_reference_formats(F, orc, gpu):
     ok, err, _ = _within(res.y, yref.view(np.float16).astype(np.float64))
     assert ok, err
     assert res.stats == F.plan_traffic(m, k, n, bits, group, workers=3)
+
+
+def test_cuda_graph_capture_without_warmup(F, orc, gpu):
+    """A fresh DeviceWeights is capture-safe for every m <= 32 (the workspace
+    is sized up front), and for larger m after reserve(); replaying the graph
+    reproduces the eager result bit for bit."""
+    rng = np.random.default_rng(12)
+    k, n, bits, group = 1024, 512, 3, 128
+    idx, sc = F.quantize_matrix(rng.standard_normal((k, n)).astype(np.float32), bits, group)
+    table = F.build_nf_table(bits)
+    st = gpu.cuda.Stream()
+    for m in (1, 4, 16, 32, 128):
+        dw = F.DeviceWeights(idx, sc, table, bits, group)
+        if m > 32:
+            dw.reserve(m)
+        x = gpu.randn(m, k, dtype=gpu.float16, device="cuda")
+        y = gpu.empty(m, n, dtype=gpu.float16, device="cuda")
+        g = gpu.cuda.CUDAGraph()
+        with gpu.cuda.graph(g, stream=st):
+            dw.gemm(x, y, stream=st.cuda_stream)
+        g.replay()
+        st.synchronize()
+        assert np.array_equal(y.cpu().numpy().view(np.uint16), dw.gemm(x).cpu().numpy().view(np.uint16))
