@@ -127,6 +127,28 @@ int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int work
 int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
                     int workers, void* stream);
 
+/* ---- weight preparation on the device / FLTE ----------
+ * flute_quantize_device: quantize_matrix (quantize.cpp:81-128) on the GPU for
+ * a device f32 [k][n] matrix -> device indices [k][n] u8 + binary16 scales
+ * [n][k/g]; bit-exact with the host quantizer; synchronises `stream`.
+ * flute_weights_from_device: a weight handle from device-resident indices +
+ * scales (packed into the device layout on the GPU); table16 = 2^bits binary16.
+ * flute_flte_info / flute_weights_from_flte: parse an FLTE container
+ * (flte.hpp:4-9, strict, FLUTE_ERR_INPUT with section + byte offset on a bad
+ * file) and upload it, canonical slices re-permuted on the GPU.
+ * flute_flte_write: indices + scales + table -> FLTE bytes (reorder_and_split
+ * at `layout`); out may be NULL to query *len. */
+int flute_quantize_device(const float* w_dev, int k, int n, int bits, int group, uint8_t* idx_dev,
+                          uint16_t* scales_dev, void* stream);
+int flute_weights_from_device(const uint8_t* idx_dev, const uint16_t* scales_dev,
+                              const uint16_t* table16, int k, int n, int bits, int group,
+                              void* stream, flute_weights** out);
+int flute_flte_info(const uint8_t* bytes, size_t len, int* bits, int* group, int* k, int* n);
+int flute_weights_from_flte(const uint8_t* bytes, size_t len, void* stream, flute_weights** out);
+int flute_flte_write(const uint8_t* indices, const uint16_t* scales, const float* table_values,
+                     int k, int n, int bits, int group, const int* layout, uint8_t* out, size_t cap,
+                     size_t* len);
+
 /* ---- N-column sharding ---------------------------------
  * Rank `rank` of `world` owns the 64-column tiles [rank*T/world,
  * (rank+1)*T/world) of T = ceil(n/64): columns [n0, n1).  Its device-layout

@@ -68,6 +68,13 @@ struct MatmulResult {
 
 MatmulResult execute(const MatmulProblem& problem);
 
+// quantize_matrix (quantize.hpp:45) on the GPU for a device-resident f32
+// [k][n] matrix: indices [k][n] and binary16 scales [n][k/g] into device
+// buffers, bit-exact with the host quantizer (synchronises `stream`; throws
+// InputError on non-finite weights or binary16 overflow).
+void quantize_on_device(const float* w_dev, int k, int n, const QuantConfig& cfg,
+                        std::uint8_t* idx_dev, std::uint16_t* scales_dev, void* stream = nullptr);
+
 double bits_per_param(const QuantConfig& cfg);
 double weight_traffic_ratio(const TrafficStats& stats, double dense_weight_bytes);
 
@@ -110,6 +117,18 @@ class DeviceWeights {
   // From a raw index matrix [k][n] + [n][k/g] scales + table values.
   DeviceWeights(const std::vector<std::uint8_t>& indices, const std::vector<Half>& scales,
                 const LookupTable& table, int k, int n, const QuantConfig& cfg);
+  // From device-resident indices [k][n] u8 + scales [n][k/g] (binary16 bits),
+  // e.g. straight out of quantize_on_device: packed into the device layout on
+  // the GPU.  `table16` are the 2^bits binary16 table values.
+  static std::unique_ptr<DeviceWeights> from_device_indices(const std::uint8_t* idx_dev,
+                                                            const std::uint16_t* scales_dev,
+                                                            const std::vector<Half>& table16, int k,
+                                                            int n, const QuantConfig& cfg,
+                                                            void* stream = nullptr);
+  // From an FLTE container (flte.hpp): the canonical slices are uploaded as
+  // stored and re-permuted to the device layout on the GPU.
+  static std::unique_ptr<DeviceWeights> from_flte(const struct FlteModel& model,
+                                                  void* stream = nullptr);
   ~DeviceWeights();
   DeviceWeights(const DeviceWeights&) = delete;
   DeviceWeights& operator=(const DeviceWeights&) = delete;
@@ -137,6 +156,7 @@ class DeviceWeights {
   struct Impl;
 
  private:
+  DeviceWeights();
   std::unique_ptr<Impl> impl_;
 };
 

@@ -232,6 +232,10 @@ class RefLib:
         L.fref_f16_to_f32.restype = C.c_float
         L.fref_f16_to_f32.argtypes = [C.c_uint16]
         L.fref_nf_table.argtypes = [C.c_int, _f32p]
+        L.fref_flte_write.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, _i32p, C.c_void_p,
+                                      C.c_size_t, C.POINTER(C.c_size_t)]
+        L.fref_flte_parse.argtypes = [_u8p, C.c_size_t, C.c_char_p, C.c_size_t,
+                                      C.POINTER(C.c_size_t)]
         L.fref_quantize.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _u16p]
         L.fref_pack.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, _i32p, _u32p, _u32p]
         L.fref_unpack.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _u32p, _u32p, _u8p]
@@ -254,6 +258,34 @@ class RefLib:
 
     def f32_to_f16(self, x: float) -> int:
         return int(self.lib.fref_f32_to_f16(float(x)))
+
+    def flte_write(self, w: np.ndarray, bits: int, group: int, layout=DEFAULT_LAYOUT) -> bytes:
+        """quantize_matrix + reorder_and_split + write_flte of the reference."""
+        w = np.ascontiguousarray(w, np.float32)
+        k, n = w.shape
+        ln = C.c_size_t(0)
+        lay = _lay(layout)
+        rc = self.lib.fref_flte_write(w, k, n, bits, group, lay, None, 0, C.byref(ln))
+        if rc:
+            raise OracleError(rc, self.lib.fref_last_error().decode())
+        out = np.zeros(ln.value, np.uint8)
+        rc = self.lib.fref_flte_write(w, k, n, bits, group, lay, out.ctypes.data, out.size,
+                                      C.byref(ln))
+        if rc:
+            raise OracleError(rc, self.lib.fref_last_error().decode())
+        return out.tobytes()
+
+    def flte_parse(self, data: bytes):
+        """None if the reference's read_flte accepts data, else (section, offset)."""
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        sec = C.create_string_buffer(64)
+        off = C.c_size_t(0)
+        rc = self.lib.fref_flte_parse(buf, buf.size, sec, 64, C.byref(off))
+        if rc == 0:
+            return None
+        if rc == 5:
+            return sec.value.decode(), off.value
+        raise OracleError(rc, self.lib.fref_last_error().decode())
 
     def nf_table(self, bits: int) -> np.ndarray:
         out = np.zeros(1 << bits, np.float32)

@@ -17,13 +17,19 @@
 //   fref_execute         -> execute                   (engine.cpp:345)
 //   fref_plan_traffic    -> plan_traffic              (engine.cpp:389)
 //   fref_f32_to_f16 / fref_f16_to_f32 -> half.hpp:81-87
+//   fref_flte_write      -> quantize + reorder_and_split + make_flte_model + write_flte (flte.cpp:80-118)
+//   fref_flte_parse      -> read_flte (flte.cpp:120-213): section / offset of a ParseError
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "flutesim/engine.hpp"
+#include "flutesim/flte.hpp"
 #include "flutesim/errors.hpp"
 #include "flutesim/half.hpp"
 #include "flutesim/nf_table.hpp"
@@ -92,6 +98,44 @@ PackedWeights packed_from(int k, int n, int bits, const int* layout,
 extern "C" {
 
 const char* fref_last_error() { return g_err.c_str(); }
+
+int fref_flte_write(const float* w, int k, int n, int bits, int group, const int* layout,
+                    std::uint8_t* out, std::size_t cap, std::size_t* len) {
+  return guarded([&] {
+    MatF m(k, n);
+    std::memcpy(m.data.data(), w, sizeof(float) * m.data.size());
+    const QuantizedMatrix q = quantize_matrix(m, QuantConfig{bits, group});
+    const LayoutDescriptor L{layout[0], layout[1], layout[2], layout[3], layout[4], layout[5]};
+    const PackedWeights pw = reorder_and_split(q, L);
+    std::ostringstream os(std::ios::binary);
+    write_flte(os, make_flte_model(q, pw));
+    const std::string b = os.str();
+    *len = b.size();
+    if (out) {
+      if (cap < b.size()) throw InputError("buffer too small");
+      std::memcpy(out, b.data(), b.size());
+    }
+  });
+}
+
+// 0 = parsed; 5 = ParseError (section copied to sec_out, offset to *off);
+// other codes as guarded().
+int fref_flte_parse(const std::uint8_t* bytes, std::size_t len, char* sec_out, std::size_t sec_cap,
+                    std::size_t* off) {
+  try {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(bytes), len), std::ios::binary);
+    (void)read_flte(is);
+    return 0;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    std::snprintf(sec_out, sec_cap, "%s", e.section.c_str());
+    *off = e.offset;
+    return 5;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
 
 std::uint16_t fref_f32_to_f16(float x) { return f32_to_f16(x).to_bits(); }
 float fref_f16_to_f32(std::uint16_t h) { return f16_to_f32(Half::from_bits(h)); }

@@ -124,6 +124,14 @@ _SIGS = {
     "flute_execute": (C.c_int, [_u16p, C.c_int, _u32p, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                 _i32p, _u16p, _u32p, C.c_int, C.c_int, C.c_int, C.c_int, _u16p,
                                 _u64p]),
+    "flute_quantize_device": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]),
+    "flute_weights_from_device": (C.c_int, [_vp, _vp, _u16p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            _vp, C.POINTER(_vp)]),
+    "flute_flte_info": (C.c_int, [_u8p, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "flute_weights_from_flte": (C.c_int, [_u8p, C.c_size_t, _vp, C.POINTER(_vp)]),
+    "flute_flte_write": (C.c_int, [_u8p, _u16p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, _i32p,
+                                   _vp, C.c_size_t, C.POINTER(C.c_size_t)]),
     "flute_shard_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(C.c_int), C.POINTER(C.c_int),
                                     C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
@@ -387,6 +395,41 @@ class DeviceWeights:
         e.g. inside CUDA-graph capture; m <= 32 never allocates)."""
         _check(_lib.flute_weights_reserve(self._h, max_m))
 
+    @classmethod
+    def _from_handle(cls, h, k, n, bits, group):
+        self = cls.__new__(cls)
+        self.k, self.n, self.bits, self.group = k, n, bits, group
+        self._h = h
+        return self
+
+    @classmethod
+    def from_device_indices(cls, idx, scales, table16: np.ndarray, bits: int, group: int,
+                            stream=None):
+        """From device-resident torch tensors: idx uint8 [k][n], scales int16/
+        uint16 bits [n*k/g] (e.g. quantize_matrix_device's outputs); packed into
+        the device layout on the GPU."""
+        k, n = idx.shape
+        h = _vp()
+        _check(_lib.flute_weights_from_device(idx.data_ptr(), scales.data_ptr(),
+                                              np.ascontiguousarray(table16, np.uint16), k, n,
+                                              bits, group, _stream_ptr(stream), C.byref(h)))
+        return cls._from_handle(h, k, n, bits, group)
+
+    @classmethod
+    def from_flte(cls, data, stream=None):
+        """From an FLTE container (bytes or a path): the canonical slices are
+        uploaded as stored and re-permuted to the device layout on the GPU."""
+        if isinstance(data, (str, os.PathLike)):
+            with open(data, "rb") as f:
+                data = f.read()
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        bits, group, k, n = (C.c_int(0) for _ in range(4))
+        _check(_lib.flute_flte_info(buf, buf.size, C.byref(bits), C.byref(group), C.byref(k),
+                                    C.byref(n)))
+        h = _vp()
+        _check(_lib.flute_weights_from_flte(buf, buf.size, _stream_ptr(stream), C.byref(h)))
+        return cls._from_handle(h, k.value, n.value, bits.value, group.value)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             _lib.flute_weights_destroy(self._h)
@@ -480,6 +523,45 @@ def execute(x16: np.ndarray, slices, k: int, n: int, bits: int, group: int, scal
                               np.ascontiguousarray(vlut_words, np.uint32), dup, workers, stages,
                               tile_m, y, st))
     return MatmulResult(y, dict(zip(TRAFFIC_FIELDS, (int(v) for v in st))))
+
+
+def quantize_matrix_device(w, bits: int, group: int, stream=None):
+    """quantize_matrix on the GPU: w torch float32 [k][n] on cuda -> (idx
+    uint8 [k][n], scales int16 [n*(k/g)] holding binary16 bits), bit-exact with
+    quantize_matrix()."""
+    import torch
+    if w.dtype != torch.float32 or not w.is_cuda or w.dim() != 2:
+        raise InputError("w must be a cuda float32 [k][n] tensor")
+    w = w.contiguous()
+    k, n = w.shape
+    idx = torch.empty((k, n), dtype=torch.uint8, device=w.device)
+    sc = torch.empty((n * (k // max(group, 1)),), dtype=torch.int16, device=w.device)
+    _check(_lib.flute_quantize_device(w.data_ptr(), k, n, bits, group, idx.data_ptr(),
+                                      sc.data_ptr(), _stream_ptr(stream)))
+    return idx, sc
+
+
+def flte_write(indices: np.ndarray, scales: np.ndarray, table_values: np.ndarray, bits: int,
+               group: int, layout=DEFAULT_LAYOUT) -> bytes:
+    """Indices + scales + table -> FLTE container bytes (flute_flte_write)."""
+    idx = np.ascontiguousarray(indices, np.uint8)
+    k, n = idx.shape
+    args = (idx, np.ascontiguousarray(scales, np.uint16),
+            np.ascontiguousarray(table_values, np.float32), k, n, bits, group, _lay(layout))
+    ln = C.c_size_t(0)
+    _check(_lib.flute_flte_write(*args, None, 0, C.byref(ln)))
+    out = np.zeros(ln.value, np.uint8)
+    _check(_lib.flute_flte_write(*args, out.ctypes.data, out.size, C.byref(ln)))
+    return out.tobytes()
+
+
+def flte_info(data: bytes):
+    """(bits, group, k, n) of an FLTE container; raises InputError (with the
+    reference's section / byte-offset message) on a malformed file."""
+    buf = np.frombuffer(bytes(data), np.uint8).copy()
+    vals = [C.c_int(0) for _ in range(4)]
+    _check(_lib.flute_flte_info(buf, buf.size, *[C.byref(v) for v in vals]))
+    return tuple(v.value for v in vals)
 
 
 @dataclass

@@ -9,6 +9,7 @@
 #include "device_api.h"
 #include "flute_c.h"
 #include "flutesim/engine.hpp"
+#include "flutesim/flte.hpp"
 #include "flutesim/errors.hpp"
 #include "flutesim/mma.hpp"
 
@@ -404,6 +405,86 @@ int flute_weights_from_indices(const uint8_t* indices, const uint16_t* scales,
     h->bits = bits;
     h->group = group;
     *out = h;
+  });
+}
+
+namespace {
+flute_weights* wrap(std::unique_ptr<DeviceWeights> dw, int k, int n, int bits, int group) {
+  auto* h = new flute_weights;
+  h->impl = dw.release();
+  h->k = k;
+  h->n = n;
+  h->bits = bits;
+  h->group = group;
+  return h;
+}
+}  // namespace
+
+int flute_quantize_device(const float* w_dev, int k, int n, int bits, int group, uint8_t* idx_dev,
+                          uint16_t* scales_dev, void* stream) {
+  return guard([&] { quantize_on_device(w_dev, k, n, QuantConfig{bits, group}, idx_dev, scales_dev, stream); });
+}
+
+int flute_weights_from_device(const uint8_t* idx_dev, const uint16_t* scales_dev,
+                              const uint16_t* table16, int k, int n, int bits, int group,
+                              void* stream, flute_weights** out) {
+  return guard([&] {
+    need(table16, "table16");
+    need(out, "out");
+    if (bits < 2 || bits > 4) throw ConfigError("bits must be in {2,3,4}");
+    std::vector<Half> t(std::size_t{1} << bits);
+    for (std::size_t i = 0; i < t.size(); ++i) t[i] = Half::from_bits(table16[i]);
+    *out = wrap(DeviceWeights::from_device_indices(idx_dev, scales_dev, t, k, n, QuantConfig{bits, group},
+                                                   stream),
+                k, n, bits, group);
+  });
+}
+
+int flute_flte_info(const uint8_t* bytes, size_t len, int* bits, int* group, int* k, int* n) {
+  return guard([&] {
+    need(bytes, "bytes");
+    const FlteModel m = parse_flte(bytes, len);
+    if (bits) *bits = m.cfg.bits;
+    if (group) *group = m.cfg.group_size;
+    if (k) *k = m.k;
+    if (n) *n = m.n;
+  });
+}
+
+int flute_weights_from_flte(const uint8_t* bytes, size_t len, void* stream, flute_weights** out) {
+  return guard([&] {
+    need(bytes, "bytes");
+    need(out, "out");
+    const FlteModel m = parse_flte(bytes, len);
+    *out = wrap(DeviceWeights::from_flte(m, stream), m.k, m.n, m.cfg.bits, m.cfg.group_size);
+  });
+}
+
+int flute_flte_write(const uint8_t* indices, const uint16_t* scales, const float* table_values,
+                     int k, int n, int bits, int group, const int* layout, uint8_t* out, size_t cap,
+                     size_t* len) {
+  return guard([&] {
+    need(indices, "indices");
+    need(scales, "scales");
+    need(table_values, "table_values");
+    need(len, "len");
+    QuantizedMatrix q;
+    q.cfg = QuantConfig{bits, group};
+    q.cfg.validate(k);
+    q.k = k;
+    q.n = n;
+    q.indices.assign(indices, indices + static_cast<size_t>(k) * n);
+    q.scales.resize(static_cast<size_t>(k / group) * n);
+    for (size_t i = 0; i < q.scales.size(); ++i) q.scales[i] = Half::from_bits(scales[i]);
+    q.table.bits = bits;
+    q.table.values.assign(table_values, table_values + (1 << bits));
+    const PackedWeights pw = reorder_and_split(q, to_layout(layout));
+    const std::vector<uint8_t> b = flte_bytes(make_flte_model(q, pw));
+    *len = b.size();
+    if (out != nullptr) {
+      if (cap < b.size()) throw InputError("flte_write: output buffer too small");
+      std::memcpy(out, b.data(), b.size());
+    }
   });
 }
 

@@ -53,6 +53,16 @@ void dequant_all(const std::uint32_t* vlut_dev_words_host, int bits, const std::
                  int n_scales, std::uint32_t* out_host);
 void mma_fragment(const std::uint16_t* a, const std::uint16_t* b, float* c, int m, int n, int k);
 
+// Weight preparation on the device (prep_kernels.cu).
+void quantize_device(const float* w, int k, int n, int bits, int group, const float* table_host,
+                     std::uint8_t* idx, std::uint16_t* scales, void* stream);
+void unpack_canonical_device(const std::uint32_t* s0, const std::uint32_t* s1, int k, int n,
+                             int bits, const int* layout6, std::uint8_t* idx, void* stream);
+void pack_device_on_device(const std::uint8_t* idx, int k, int n, int bits, int group,
+                           std::uint8_t* out, void* stream);
+void scales_device_on_device(const std::uint16_t* sc, int k, int n, int group,
+                             std::uint16_t* out, void* stream);
+
 // Small RAII device buffer helpers used by the host layer.
 void* dev_alloc(std::size_t bytes);
 void dev_free(void* p);

@@ -7,6 +7,8 @@
 
 #include "device_api.h"
 #include "flutesim/engine.hpp"
+#include "flutesim/flte.hpp"
+#include "flutesim/nf_table.hpp"
 #include "flutesim/errors.hpp"
 #include "flutesim/mma.hpp"
 
@@ -214,6 +216,69 @@ DeviceWeights::DeviceWeights(const std::vector<std::uint8_t>& indices,
   impl_->upload(pack_device(indices, k, n, cfg.bits, cfg.group_size),
                 scales_to_device(scales, k, n, cfg.group_size),
                 device_vlut_words(make_vectorized_lut(table, 1)));
+}
+
+DeviceWeights::DeviceWeights() : impl_(std::make_unique<Impl>()) {}
+
+std::unique_ptr<DeviceWeights> DeviceWeights::from_device_indices(
+    const std::uint8_t* idx_dev, const std::uint16_t* scales_dev, const std::vector<Half>& table16,
+    int k, int n, const QuantConfig& cfg, void* stream) {
+  cfg.validate(k);
+  if (idx_dev == nullptr || scales_dev == nullptr) throw InputError("null device indices/scales");
+  if (table16.size() != (std::size_t{1} << cfg.bits)) throw ConfigError("table size != 2^bits");
+  const DeviceGeometry g = device_geometry(k, n, cfg.bits, cfg.group_size);
+  std::unique_ptr<DeviceWeights> dw(new DeviceWeights());
+  Impl& im = *dw->impl_;
+  im.k = k;
+  im.n = n;
+  im.bits = cfg.bits;
+  im.group = cfg.group_size;
+  im.w = DeviceBuffer(g.weight_bytes());
+  im.sc = DeviceBuffer(g.scale_bytes());
+  flute_dev::pack_device_on_device(idx_dev, k, n, cfg.bits, cfg.group_size,
+                                   static_cast<std::uint8_t*>(im.w.p), stream);
+  flute_dev::scales_device_on_device(scales_dev, k, n, cfg.group_size,
+                                     static_cast<std::uint16_t*>(im.sc.p), stream);
+  LookupTable t;
+  t.bits = cfg.bits;
+  for (const Half h : table16) t.values.push_back(f16_to_f32(h));
+  const std::vector<std::uint32_t> words = device_vlut_words(make_vectorized_lut(t, 1));
+  im.lut = DeviceBuffer(words.size() * 4);
+  flute_dev::h2d(im.lut.p, words.data(), words.size() * 4, stream);
+  flute_dev::stream_sync(stream);
+  im.reserve(32);
+  return dw;
+}
+
+std::unique_ptr<DeviceWeights> DeviceWeights::from_flte(const FlteModel& model, void* stream) {
+  const int k = model.k, n = model.n, bits = model.cfg.bits;
+  const std::size_t words0 = model.slices.at(0).words.size();
+  const std::size_t words1 = bits == 3 ? model.slices.at(1).words.size() : 0;
+  DeviceBuffer s0(words0 * 4), s1(words1 * 4 + 4), idx(static_cast<std::size_t>(k) * n),
+      sc(model.scales.size() * 2);
+  flute_dev::h2d(s0.p, model.slices[0].words.data(), words0 * 4, stream);
+  if (bits == 3) flute_dev::h2d(s1.p, model.slices[1].words.data(), words1 * 4, stream);
+  flute_dev::h2d(sc.p, model.scales.data(), model.scales.size() * 2, stream);
+  const LayoutDescriptor& L = model.layout;
+  const int lay[6] = {L.tile_m, L.tile_n, L.tile_k, L.frag_m, L.frag_n, L.frag_k};
+  flute_dev::unpack_canonical_device(static_cast<const std::uint32_t*>(s0.p),
+                                     static_cast<const std::uint32_t*>(s1.p), k, n, bits, lay,
+                                     static_cast<std::uint8_t*>(idx.p), stream);
+  auto dw = from_device_indices(static_cast<const std::uint8_t*>(idx.p),
+                                static_cast<const std::uint16_t*>(sc.p), model.table, k, n,
+                                model.cfg, stream);
+  return dw;  // (from_device_indices synchronised the stream before the temporaries go)
+}
+
+void quantize_on_device(const float* w_dev, int k, int n, const QuantConfig& cfg,
+                        std::uint8_t* idx_dev, std::uint16_t* scales_dev, void* stream) {
+  cfg.validate(k);
+  if (n < 1) throw ConfigError("quantize: n must be positive");
+  if (w_dev == nullptr || idx_dev == nullptr || scales_dev == nullptr)
+    throw InputError("quantize: null device pointer");
+  const LookupTable t = build_nf_table(cfg.bits);
+  flute_dev::quantize_device(w_dev, k, n, cfg.bits, cfg.group_size, t.values.data(), idx_dev,
+                             scales_dev, stream);
 }
 
 DeviceWeights::~DeviceWeights() = default;
