@@ -223,6 +223,8 @@ BASE = [  # BASELINE.json configs at full size (parity by the same bound)
     (1, 4096, 4096, 4, 128), (16, 4096, 4096, 4, 128),
     (1, 4096, 14336, 3, 128), (32, 4096, 14336, 3, 128), (4, 14336, 4096, 3, 128),
     (1, 8192, 8192, 2, 256), (8, 8192, 8192, 4, 32),
+    (1, 8192, 28672, 4, 128),                        # configs[3] layer (1 GPU)
+    (128, 4096, 4096, 4, 128), (512, 2048, 4096, 4, 128),  # configs[4] (tcgen05 path)
 ]
 
 

@@ -66,7 +66,9 @@ __global__ void lds_lut(int iters, float* out) {
 
 // The LUT-GEMM inner loop in isolation: per iteration each warp loads 16 B of
 // packed W4 indices + a scale word vector + an X fragment from shared memory,
-// then dequantises 4 atoms (4 x PRMT->LDS->HMUL2) and issues 4 HMMAs.
+// then dequantises ATOMS atoms (4 x PRMT->LDS->HMUL2) and issues HMMAs.
+// VAR: 0 full, 1 no HMUL2, 2 no vLUT LDS (index bytes used as data), 3 no HMMA.
+template <int VAR, int ATOMS>
 __global__ void lut_mma_loop(int iters, float* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint32_t* w = reinterpret_cast<uint32_t*>(sm);
@@ -77,36 +79,49 @@ __global__ void lut_mma_loop(int iters, float* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lane4 = lane * 4;
   float acc[4][4] = {};
+  uint32_t sink = 0;
   for (int i = 0; i < iters; ++i) {
-    const uint32_t off = data + ((i * 8 + warp) & 63) * 512;
-    uint4 lb, sq;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(lb.x), "=r"(lb.y), "=r"(lb.z), "=r"(lb.w) : "r"(off + lane * 16));
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(sq.x), "=r"(sq.y), "=r"(sq.z), "=r"(sq.w) : "r"(off + (lane >> 2) * 16));
-    uint32_t b0, b1;
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(off + (lane & 15) * 16));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t idx = j == 0 ? lb.x : j == 1 ? lb.y : j == 2 ? lb.z : lb.w;
-      const uint32_t scw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
-      const __half2 s2 = *reinterpret_cast<const __half2*>(&scw);
-      uint32_t a[4];
+    for (int h = 0; h < ATOMS / 4; ++h) {
+      const uint32_t off = data + ((i * 8 + warp + h * 3) & 63) * 512;
+      uint4 lb, sq;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(lb.x), "=r"(lb.y), "=r"(lb.z), "=r"(lb.w) : "r"(off + lane * 16));
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(sq.x), "=r"(sq.y), "=r"(sq.z), "=r"(sq.w) : "r"(off + (lane >> 2) * 16));
+      uint32_t b0, b1;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(off + (lane & 15) * 16));
 #pragma unroll
-      for (int pp = 0; pp < 4; ++pp) {
-        uint32_t o;
-        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(o) : "r"(idx), "r"(lane4), "r"(0x5504u | (pp << 4)));
-        uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut + o));
-        const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v), (pp & 1) ? __high2half2(s2) : __low2half2(s2));
-        a[pp] = *reinterpret_cast<const uint32_t*>(&r);
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t idx = j == 0 ? lb.x : j == 1 ? lb.y : j == 2 ? lb.z : lb.w;
+        const uint32_t scw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
+        const __half2 s2 = *reinterpret_cast<const __half2*>(&scw);
+        uint32_t a[4];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+          uint32_t o;
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(o) : "r"(idx), "r"(lane4), "r"(0x5504u | (pp << 4)));
+          uint32_t v;
+          if (VAR == 2) v = o;
+          else asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut + o));
+          if (VAR == 1) {
+            a[pp] = v;
+          } else {
+            const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v), (pp & 1) ? __high2half2(s2) : __low2half2(s2));
+            a[pp] = *reinterpret_cast<const uint32_t*>(&r);
+          }
+        }
+        if (VAR == 3) {
+          sink ^= a[0] ^ a[1] ^ a[2] ^ a[3] ^ b0 ^ b1;
+        } else {
+          asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                       : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
+                       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+        }
       }
-      asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-                   : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
-                   : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
     }
   }
   float s = 0.f;
   for (int j = 0; j < 4; ++j) for (int r = 0; r < 4; ++r) s += acc[j][r];
-  if (s == 1.2345f) out[0] = s;
+  if (s == 1.2345f || sink == 0x1234567u) out[0] = s;
 }
 
 // mbarrier costs: (a) try_wait on an already-completed phase, (b) a
@@ -206,8 +221,16 @@ int main() {
     mbar_latency<<<1, 160>>>(10000, o);
     cudaDeviceSynchronize();
   }
-  for (int th : {128, 256, 512, 1024})
-    run("lut+mma atom (per warp-atom)", lut_mma_loop, th, 65536 + 32768 + 1024, 4.0, "T atoms/s", it / 4);
+  const size_t sm = 65536 + 32768 + 1024;
+  for (int th : {256, 512}) {
+    run("full, 4 atoms/iter", lut_mma_loop<0, 4>, th, sm, 4.0, "T atoms/s", it / 4);
+    run("full, 8 atoms/iter", lut_mma_loop<0, 8>, th, sm, 8.0, "T atoms/s", it / 8);
+    run("full, 16 atoms/iter", lut_mma_loop<0, 16>, th, sm, 16.0, "T atoms/s", it / 16);
+    run("no HMUL2, 8", lut_mma_loop<1, 8>, th, sm, 8.0, "T atoms/s", it / 8);
+    run("no vLUT LDS, 8", lut_mma_loop<2, 8>, th, sm, 8.0, "T atoms/s", it / 8);
+    run("no HMMA, 8", lut_mma_loop<3, 8>, th, sm, 8.0, "T atoms/s", it / 8);
+  }
+  return 0;
   for (int th : {128, 256, 512, 1024}) {
     run("hmma f32acc 1 chain", hmma_f32<1>, th, 0, 4096.0, "TFLOP/s", it);
     run("hmma f32acc 4 chains", hmma_f32<4>, th, 0, 4 * 4096.0, "TFLOP/s", it);
