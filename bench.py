@@ -237,6 +237,17 @@ def run_ours(args):
             xs[(m, k)] = x
     ys = {(m, n): torch.empty((m, n), dtype=torch.float16, device="cuda")
           for m in MS for (_, n) in SHAPES}
+    # load-time autotuning (public API; outside the timed region): pick the
+    # work decomposition per weight handle and row class
+    tuned = {}
+    if args.autotune:
+        for (k, n), reps in weights.items():
+            for m in MS:
+                for dw in reps:
+                    r = dw.autotune(m)
+                tuned[f"M={m} K={k} N={n}"] = min(
+                    (ln for ln in r.splitlines() if ln.strip()),
+                    key=lambda ln: float(ln.split(":")[-1].split()[0]))
     cases = [(m, k, n) for m in MS for (k, n) in SHAPES]
     step_bytes = sum(algo_bytes(m, k, n) for (m, k, n) in cases)
 
@@ -371,7 +382,8 @@ def run_ours(args):
                        "l2": f"inputs larger than L2: {REPLICAS} weight replicas per shape "
                              "rotated per launch",
                        "parallelism": f"weak: {world} GPU(s) each run the full per-GPU workload",
-                       "step_bytes": step_bytes, "timing": "CUDA graph of 16 steps, events"},
+                       "step_bytes": step_bytes, "timing": "CUDA graph of 16 steps, events",
+                       "autotune": tuned or "off"},
             "roofline": {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(value / world / peak, 4),
                          "peak_kind": peak_kind,
@@ -475,6 +487,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--quick", action="store_true", help="skip per-case micro-benchmarks")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--autotune", action="store_true",
+                    help="run DeviceWeights.autotune per handle and row class at load time "
+                         "(isolated cold-launch criterion; the heuristic matches it on this workload)")
     ap.add_argument("--workload", default="mlp8b", choices=["mlp8b", "70b"],
                     help="mlp8b: configs[1] (default, weak scaling); 70b: configs[3] N-sharded")
     ap.add_argument("--allgather", default="nccl", choices=["nccl", "peer"])

@@ -120,6 +120,11 @@ int flute_weights_destroy(flute_weights* w);
 /* Pre-size the handle's device workspace for calls with m <= max_m so that no
  * later flute_gemm allocates (required before CUDA-graph capture of m > 32). */
 int flute_weights_reserve(flute_weights* w, int max_m);
+/* Time the candidate work decompositions (cluster split-K sizes, Stream-K CTA
+ * counts) for m-row calls (1 <= m <= 32) on this handle's shape, L2 flushed
+ * between runs, and keep the fastest for later workers <= 0 calls of the same
+ * row class; `report` (nullable) receives the timings. */
+int flute_weights_autotune(flute_weights* w, int m, void* stream, char* report, size_t cap);
 int flute_weights_info(const flute_weights* w, int* k, int* n, int* bits, int* group);
 int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int workers,
                void* stream);

@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <string>
 
 #include "flutesim/matrix.hpp"
 #include "flutesim/pack.hpp"
@@ -139,6 +140,12 @@ class DeviceWeights {
   // so no later call allocates (e.g. inside CUDA-graph capture).  Calls with
   // m <= 32 never allocate; larger m (tcgen05 split-K partials) may on first use.
   void reserve(int max_m);
+  // Time the candidate decompositions (cluster split-K sizes, Stream-K worker
+  // counts) for m-row calls on this weight shape and keep the fastest for
+  // later default-worker calls of the same row class (M <= 8 / 16 / 32);
+  // returns the timing report.  The paper's "compile several instantiations,
+  // keep the best", at run time.
+  std::string autotune(int m, void* stream = nullptr, int reps = 20);
   // y_dev[m][n] = x_dev[m][k] * W_hat, device pointers, async on `stream`.
   void gemm(const Half* x_dev, int m, Half* y_dev, int workers = 0, void* stream = nullptr);
   // N-sharded layer: store this GEMM's [m][n] result into every y_peers[i]

@@ -117,6 +117,7 @@ _SIGS = {
                                              C.c_int, C.POINTER(_vp)]),
     "flute_weights_destroy": (C.c_int, [_vp]),
     "flute_weights_reserve": (C.c_int, [_vp, C.c_int]),
+    "flute_weights_autotune": (C.c_int, [_vp, C.c_int, _vp, C.c_char_p, C.c_size_t]),
     "flute_weights_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "flute_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _vp]),
@@ -429,6 +430,14 @@ class DeviceWeights:
         h = _vp()
         _check(_lib.flute_weights_from_flte(buf, buf.size, _stream_ptr(stream), C.byref(h)))
         return cls._from_handle(h, k.value, n.value, bits.value, group.value)
+
+    def autotune(self, m: int, stream=None) -> str:
+        """Time the candidate decompositions for m-row calls (L2 flushed) and
+        keep the fastest for this handle's default-worker calls of that row
+        class (M <= 8 / 16 / 32).  Returns the timing report."""
+        buf = C.create_string_buffer(4096)
+        _check(_lib.flute_weights_autotune(self._h, m, _stream_ptr(stream), buf, 4096))
+        return buf.value.decode()
 
     def close(self) -> None:
         if getattr(self, "_h", None):

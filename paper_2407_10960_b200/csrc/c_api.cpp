@@ -2,6 +2,7 @@
 // point converts plain pointers to the C++ API and maps exceptions to status
 // codes, keeping the message for flute_last_error().
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -503,6 +504,14 @@ int flute_weights_info(const flute_weights* w, int* k, int* n, int* bits, int* g
     if (n) *n = w->n;
     if (bits) *bits = w->bits;
     if (group) *group = w->group;
+  });
+}
+
+int flute_weights_autotune(flute_weights* w, int m, void* stream, char* report, size_t cap) {
+  return guard([&] {
+    need(w, "weights");
+    const std::string r = w->impl->autotune(m, stream);
+    if (report && cap > 0) std::snprintf(report, cap, "%s", r.c_str());
   });
 }
 

@@ -5,6 +5,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
+#include <vector>
 
 namespace flute_dev {
 
@@ -26,7 +28,21 @@ struct GemmArgs {
   std::size_t workspace_bytes = 0;
   int workers = 0;               // <= 0: default
   void* stream = nullptr;
+  // Decomposition override (autotuner): cluster >= 1 forces cluster split-K
+  // with that cluster size (workers ignored); 0 = Stream-K with `workers`;
+  // -1 = heuristic.
+  int cluster = -1;
 };
+
+// Candidate decompositions for an m-row call (autotuner): {cluster, workers}.
+struct Decomp {
+  int cluster = -1, workers = 0;
+};
+std::vector<Decomp> decomp_candidates(int m, int k, int n);
+// Mean device time (us) of `fn` (one launch sequence on `stream`), each rep
+// preceded by an untimed write of a buffer larger than L2 so weights stream
+// from HBM as in real use.
+double time_launches(const std::function<void()>& fn, int reps, void* stream);
 
 void qgemm(const GemmArgs& a);
 

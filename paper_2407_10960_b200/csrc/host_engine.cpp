@@ -157,8 +157,14 @@ struct DeviceWeights::Impl {
     }
   }
 
+  // autotuned decomposition per m-class (row block 8 / 16 / 32), -1 = none
+  flute_dev::Decomp tuned[3] = {};
+
+  static int mclass(int m) { return m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : -1; }
+
   void gemm(const void* x, int m, void* y, int workers, void* stream,
-            void* const* y_peers = nullptr, int n_peers = 0, int ldy = 0, int ycol0 = 0) {
+            void* const* y_peers = nullptr, int n_peers = 0, int ldy = 0, int ycol0 = 0,
+            const flute_dev::Decomp* force = nullptr) {
     const std::size_t need = flute_dev::call_workspace_bytes(m, k, n, workers);
     if (need > ws.bytes) {
       ws = DeviceBuffer(need);
@@ -184,6 +190,12 @@ struct DeviceWeights::Impl {
     a.n_peers = n_peers;
     a.ldy = ldy;
     a.ycol0 = ycol0;
+    const int mc = mclass(m);
+    const flute_dev::Decomp* d = force ? force : (workers <= 0 && mc >= 0 ? &tuned[mc] : nullptr);
+    if (d && d->cluster >= 0) {
+      a.cluster = d->cluster;
+      a.workers = d->cluster == 0 ? d->workers : 0;
+    }
     flute_dev::qgemm(a);
   }
 };
@@ -284,6 +296,42 @@ void quantize_on_device(const float* w_dev, int k, int n, const QuantConfig& cfg
 DeviceWeights::~DeviceWeights() = default;
 int DeviceWeights::k() const { return impl_->k; }
 void DeviceWeights::reserve(int max_m) { impl_->reserve(max_m); }
+
+std::string DeviceWeights::autotune(int m, void* stream, int reps) {
+  Impl& im = *impl_;
+  const int mc = Impl::mclass(m);
+  if (mc < 0) throw ConfigError("autotune: m must be in [1, 32] (the memory-bound kernel)");
+  if (reps < 1) reps = 1;
+  DeviceBuffer x(static_cast<std::size_t>(m) * im.k * 2), y(static_cast<std::size_t>(m) * im.n * 2);
+  flute_dev::dev_zero(x.p, x.bytes, stream);
+  const std::vector<flute_dev::Decomp> cands = flute_dev::decomp_candidates(m, im.k, im.n);
+  for (const flute_dev::Decomp& c : cands) {  // grow the workspace before timing
+    if (c.cluster == 0) {
+      const std::size_t need = flute_dev::workspace_bytes(m, c.workers);
+      if (need > im.ws.bytes) {
+        im.ws = DeviceBuffer(need);
+        flute_dev::dev_zero(im.ws.p, im.ws.bytes, nullptr);
+        flute_dev::stream_sync(nullptr);
+      }
+    }
+  }
+  double best_t = 1e30;
+  flute_dev::Decomp best{};
+  std::string report;
+  for (const flute_dev::Decomp& c : cands) {
+    auto run = [&] { im.gemm(x.p, m, y.p, 0, stream, nullptr, 0, 0, 0, &c); };
+    for (int i = 0; i < 3; ++i) run();
+    const double t = flute_dev::time_launches(run, reps, stream);
+    report += "cluster=" + std::to_string(c.cluster) + " workers=" + std::to_string(c.workers) +
+              ": " + std::to_string(t) + " us\n";
+    if (t < best_t) {
+      best_t = t;
+      best = c;
+    }
+  }
+  im.tuned[mc] = best;
+  return report;
+}
 int DeviceWeights::n() const { return impl_->n; }
 
 void DeviceWeights::gemm(const Half* x_dev, int m, Half* y_dev, int workers, void* stream) {

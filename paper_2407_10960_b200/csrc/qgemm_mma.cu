@@ -347,6 +347,47 @@ size_t workspace_bytes(int m, int workers) {
   return flag_span + static_cast<size_t>(workers) * (bm / 8) * 16 * 32 * 4;
 }
 
+double time_launches(const std::function<void()>& fn, int reps, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int l2 = 0, dev = 0;
+  FLUTE_CUDA(cudaGetDevice(&dev));
+  FLUTE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+  const size_t flush_bytes = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
+  void* flush = nullptr;
+  FLUTE_CUDA(cudaMalloc(&flush, flush_bytes));
+  cudaEvent_t e0, e1;
+  FLUTE_CUDA(cudaEventCreate(&e0));
+  FLUTE_CUDA(cudaEventCreate(&e1));
+  double total_ms = 0;
+  for (int r = 0; r < reps; ++r) {
+    FLUTE_CUDA(cudaMemsetAsync(flush, r & 0xFF, flush_bytes, st));
+    FLUTE_CUDA(cudaEventRecord(e0, st));
+    fn();
+    FLUTE_CUDA(cudaEventRecord(e1, st));
+    FLUTE_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    FLUTE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    total_ms += ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(flush);
+  return total_ms * 1e3 / reps;
+}
+
+std::vector<Decomp> decomp_candidates(int m, int k, int n) {
+  std::vector<Decomp> out;
+  const int tiles_k = (k + kUnitK - 1) / kUnitK;
+  const long long tiles_n = (n + kUnitN - 1) / kUnitN;
+  const int slots = max_workers(std::min(m, 32));
+  out.push_back({-1, 0});  // the heuristic's own choice
+  for (int c = 1; c <= 8; c *= 2)
+    if (c <= tiles_k && tiles_n * c <= slots && 2 * tiles_n * c >= slots) out.push_back({c, 0});
+  for (const int w : {props().sms, slots})
+    if (w <= tiles_k * tiles_n) out.push_back({0, w});
+  return out;
+}
+
 size_t call_workspace_bytes(int m, int k, int n, int workers) {
   const size_t mma = workspace_bytes(std::min(m, 32), workers > 0 ? workers : max_workers(std::min(m, 32)) * 4);
   return tc_enabled(m) ? std::max(mma, tc_workspace_bytes(m, k, n, props().sms)) : mma;
@@ -374,7 +415,11 @@ void qgemm(const GemmArgs& a) {
   const long long units = static_cast<long long>(tiles_k) * (np / kUnitN);
   // default: cluster split-K when the tile count suits it, else Stream-K over
   // min(units, #SMs) CTAs; an explicit worker count always means Stream-K
-  int cluster = a.workers > 0 ? 0 : cluster_for(np / kUnitN, tiles_k, a.m);
+  int cluster = a.cluster >= 1   ? std::min(a.cluster, tiles_k)
+                : a.cluster == 0 ? 0
+                : a.workers > 0  ? 0
+                                 : cluster_for(np / kUnitN, tiles_k, a.m);
+  if (a.cluster == 0 && a.workers <= 0) cluster = 0;
   int workers = cluster > 0 ? static_cast<int>(np / kUnitN) * cluster
                             : (a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits));
   if (units * (static_cast<long long>(workers) + 1) >= (1LL << 31))

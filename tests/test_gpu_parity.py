@@ -338,3 +338,21 @@ def test_cuda_graph_capture_without_warmup(F, orc, gpu):
         g.replay()
         st.synchronize()
         assert np.array_equal(y.cpu().numpy().view(np.uint16), dw.gemm(x).cpu().numpy().view(np.uint16))
+
+
+def test_autotune_keeps_results_in_bound(F, orc, gpu):
+    """autotune() times the candidate decompositions and keeps the fastest;
+    later default calls stay within the bound and bitwise reproducible."""
+    rng = np.random.default_rng(8)
+    m, k, n, bits, group = 4, 2048, 1024, 3, 128
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    dw = F.DeviceWeights(idx, scales, table, bits, group)
+    report = dw.autotune(m)
+    assert report.count("us") >= 2, report
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    y1 = dw.gemm(x).cpu().numpy().view(np.uint16)
+    y2 = dw.gemm(x).cpu().numpy().view(np.uint16)
+    assert np.array_equal(y1, y2)
+    assert _within(y1, orc.reference_f64(x16, idx, bits, group, scales, table))[0]
+    with pytest.raises(F.ConfigError):
+        dw.autotune(64)
