@@ -195,9 +195,11 @@ int flute_dequant_all_device(const uint32_t* vlut_words, int bits, const uint16_
 /* Diagnostics (libflute_b200_diag.so only; `make diag`): with
  * FLUTE_DEBUG_TIMES=1, each qgemm launch records per-CTA %globaltimer stamps
  * (ns) {start, producer issued, LUT ready, first stage landed, segment end,
- * last segment end, exit, finisher acquired} (8*workers values) followed by a
- * per-stage trace of consumer warp 0 (workers*64*3 values: wait begin, data
- * ready, compute done); copies all 200*workers values of the last launch. */
+ * last segment end, exit, finisher acquired} plus {after the CTA barrier,
+ * producer policy set, producer PDL wait done, vLUT filled, epilogue PDL wait
+ * done} (16*workers values) followed by a per-stage trace of consumer warp 0
+ * (workers*64*3 values: wait begin, data ready, compute done); copies all
+ * 208*workers values of the last launch. */
 int flute_debug_times(uint64_t* out, int workers);
 /* mma_fragment on the tensor cores (mma.hpp:23); host buffers. */
 int flute_mma_fragment(const uint16_t* a, const uint16_t* b, float* c, int m, int n, int k);

@@ -615,9 +615,9 @@ def mma_fragment(a16: np.ndarray, b16: np.ndarray, c: np.ndarray) -> np.ndarray:
 
 def debug_times(workers: int) -> np.ndarray:
     """Per-CTA ns timeline of the last launch (needs FLUTE_DEBUG_TIMES=1)."""
-    out = np.zeros(200 * workers, np.uint64)
+    out = np.zeros(208 * workers, np.uint64)
     _check(_lib.flute_debug_times(out, workers))
-    return out[:8 * workers].reshape(workers, 8), out[8 * workers:].reshape(workers, 64, 3)
+    return out[:16 * workers].reshape(workers, 16), out[16 * workers:].reshape(workers, 64, 3)
 
 
 def exported_symbols() -> Sequence[str]:

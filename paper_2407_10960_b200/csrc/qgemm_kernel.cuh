@@ -126,7 +126,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifdef FLUTE_DIAGNOSTICS
 #define FLUTE_STAMP(slot)                                                     \
   do {                                                                        \
-    if (p.dbg) p.dbg[static_cast<size_t>(blockIdx.x) * 8 + (slot)] = gtimer(); \
+    if (p.dbg) p.dbg[static_cast<size_t>(blockIdx.x) * 16 + (slot)] = gtimer(); \
   } while (0)
 #define FLUTE_DIAG(bit) ((p.diag & (bit)) != 0)
 #else
@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
   }
   __syncthreads();
   if (p.use_ticket) wid = static_cast<int>(misc[0]);
+  if (threadIdx.x == 0) FLUTE_STAMP(8);
   // cluster mode: the receive barrier must be initialised before any peer
   // arrives on it (waited for just before the first remote access)
   if (p.cluster > 1) cluster_arrive_relaxed();
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
       const bool leader = elect_one();
       if (leader) prefetch_tmap(&tmap_x);
       const uint64_t pol = policy_evict_first();
+      if (lane == 0) FLUTE_STAMP(9);
       const bool do_w = !FLUTE_DIAG(2), do_x = !FLUTE_DIAG(4), do_s = !FLUTE_DIAG(8);
       // stage = units [t*tiles_k + lo, t*tiles_k + lo + ns) of tile t
       auto issue_ws = [&](int t, int lo, int ns, int s) {
@@ -302,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
       }
       FLUTE_STAMP(1);
       if (!p.use_ticket) pdl_wait();  // X and the workspace belong to the previous kernel
+      if (lane == 0) FLUTE_STAMP(10);
       Ring ring;
       int it = 0;
       for (int t = R.t_hi; t >= R.t_lo; --t) {
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
   } else if (warp == kEpilogueWarp) {
     // ===================== epilogue =====================
     if (!p.use_ticket) pdl_wait();  // the workspace and Y belong to the previous kernel
+    if (lane == 0) FLUTE_STAMP(12);
     int seg = 0;
     for (int tile = R.t_hi; uend > ubeg && tile >= R.t_lo; --tile, ++seg) {
       // fixed-order sum of the 8 warp partials, then free the buffer
@@ -451,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
   } else {
     // ===================== consumers =====================
     if (!FLUTE_DIAG(32)) fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
+    if (threadIdx.x == 0) FLUTE_STAMP(11);
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
     // Two halves of 4 warps take alternate stages (half h: stages i with
     // i % 2 == h), so the two warps sharing an SMSP are out of phase (one in
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
     int stage_no = 0;
     unsigned long long* trace =
         (p.dbg && threadIdx.x == 0)
-            ? p.dbg + static_cast<size_t>(gridDim.x) * 8 + static_cast<size_t>(blockIdx.x) * 64 * 3
+            ? p.dbg + static_cast<size_t>(gridDim.x) * 16 + static_cast<size_t>(blockIdx.x) * 64 * 3
             : nullptr;
 #endif
 

@@ -110,7 +110,7 @@ const DevProps& props() {
 // producer issued, LUT ready, first stage ready, segment end, last segment
 // end, exit, finisher acquired} followed by a per-stage trace of consumer
 // warp 0: 64 stages x {wait begin, data ready, compute done}.
-constexpr size_t kDbgPerCta = 8 + 64 * 3;
+constexpr size_t kDbgPerCta = 16 + 64 * 3;
 unsigned long long* g_dbg = nullptr;
 int g_dbg_cap = 0;
 unsigned long long* debug_times_buffer(int workers) {

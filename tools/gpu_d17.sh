@@ -1,0 +1,2 @@
+export FLUTE_LIB=paper_2407_10960_b200/libflute_b200_diag.so
+for d in 15 0; do echo "== DIAG=$d"; FLUTE_DIAG=$d timeout 100 python tools/timeline.py 1 4096 14336 3 128 --stages; done

@@ -127,13 +127,17 @@ __global__ void lut_mma_loop(int iters, float* out) {
 // mbarrier costs: (a) try_wait on an already-completed phase, (b) a
 // producer/consumer ping-pong through a ring of S barriers (no data).
 __global__ void mbar_latency(int iters, float* out) {
-  __shared__ __align__(8) unsigned long long bars[64];
+  __shared__ __align__(8) unsigned long long bars[128];
   const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 32; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 8 * i), "r"(1) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 256 + 8 * i), "r"(4) : "memory");
+    }
+    for (int i = 0; i < 8; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 512 + 8 * i), "r"(1) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 576 + 8 * i), "r"(4) : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -162,7 +166,7 @@ __global__ void mbar_latency(int iters, float* out) {
   }
   __syncthreads();
   // (b) ring ping-pong: warp 0 = producer (waits empty, arrives full), warps 1..4 consumers
-  const int S = 4;
+  const int S = out ? 4 : 4;
   if (warp == 0) {
     t0 = clock64();
     for (int i = 0, s = 0, ph = 0; i < iters; ++i) {
@@ -186,7 +190,95 @@ __global__ void mbar_latency(int iters, float* out) {
       if (++s == S) { s = 0; ph ^= 1; }
     }
   }
+  __syncthreads();
+  // (b) ring ping-pong: warp 0 = producer (waits empty, arrives full), warps 1..4 consumers
+  const int S3 = 4;
+  if (warp == 0) {
+    t0 = clock64();
+    for (int i = 0, s = 0, ph = 0; i < iters; ++i) {
+      if (i >= S3) {
+        uint32_t ok = 0;
+        while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(ok) : "r"(b0 + 576 + 8 * s), "r"(ph ^ 1u) : "memory");
+      }
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b0 + 512 + 8 * s) : "memory");
+      if (++s == S3) { s = 0; ph ^= 1; }
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) printf("  ring of %d, sink-form arrive: %.1f cycles/stage\n", S3, double(t1 - t0) / iters);
+  } else if (warp <= 4) {
+    for (int i = 0, s = 0, ph = 0; i < iters; ++i) {
+      uint32_t ok = 0;
+      while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                               : "=r"(ok) : "r"(b0 + 512 + 8 * s), "r"(ph) : "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b0 + 576 + 8 * s) : "memory");
+      if (++s == S3) { s = 0; ph ^= 1; }
+    }
+  }
+  __syncthreads();
+  // (b) ring ping-pong: warp 0 = producer (waits empty, arrives full), warps 1..4 consumers
+  const int S2 = 4;
+  if (warp == 0) {
+    t0 = clock64();
+    for (int i = 0, s = 0, ph = 0; i < iters; ++i) {
+      if (i >= S2) {
+        uint32_t ok = 0;
+        while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(ok) : "r"(b0 + 256 + 8 * (s + 16)), "r"(ph ^ 1u) : "memory");
+      }
+      if (lane == 0) asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(b0 + 8 * (s + 16)) : "memory");
+      if (++s == S2) { s = 0; ph ^= 1; }
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) printf("  ring of %d (test_wait spin): %.1f cycles/stage\n", S2, double(t1 - t0) / iters);
+  } else if (warp <= 4) {
+    for (int i = 0, s = 0, ph = 0; i < iters; ++i) {
+      uint32_t ok = 0;
+      while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                               : "=r"(ok) : "r"(b0 + 8 * (s + 16)), "r"(ph) : "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(b0 + 256 + 8 * (s + 16)) : "memory");
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+  }
   if (iters == -7) out[0] = 1.f;
+}
+
+// Per-op issue cost of mbarrier.arrive.expect_tx and cp.async.bulk from one
+// thread (barriers re-initialised each round so phases always complete).
+__global__ void arrive_cost(const uint8_t* src, float* out) {
+  __shared__ __align__(8) unsigned long long bars[16];
+  __shared__ __align__(128) uint8_t buf[16 * 1024];
+  const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  const uint32_t d0 = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+  if (threadIdx.x != 0) return;
+  long long t_init = 0, t_arr = 0, t_tx = 0, t_bulk = 0;
+  for (int round = 0; round < 20; ++round) {
+    long long t0 = clock64();
+    for (int i = 0; i < 16; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 8 * i), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    long long t1 = clock64();
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b0 + 8 * i) : "memory");
+    long long t2 = clock64();
+    for (int i = 8; i < 16; ++i)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b0 + 8 * i), "r"(1024u) : "memory");
+    long long t3 = clock64();
+    for (int i = 8; i < 16; ++i)
+      asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d0 + (i - 8) * 1024),
+                   "l"(src + (round * 16 + i) * 4096), "r"(1024u), "r"(b0 + 8 * i) : "memory");
+    long long t4 = clock64();
+    for (int i = 8; i < 16; ++i) {
+      uint32_t ok = 0;
+      while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(b0 + 8 * i), "r"(0u) : "memory");
+    }
+    if (round > 0) { t_init += t1 - t0; t_arr += t2 - t1; t_tx += t3 - t2; t_bulk += t4 - t3; }
+  }
+  printf("  per op (cycles): mbarrier.init %.1f | arrive %.1f | arrive.expect_tx %.1f | cp.async.bulk 1KB issue %.1f\n",
+         t_init / (19.0 * 16), t_arr / (19.0 * 8), t_tx / (19.0 * 8), t_bulk / (19.0 * 8));
+  out[0] = 0.f;
 }
 
 template <class K>
@@ -219,6 +311,10 @@ int main() {
     float* o;
     cudaMalloc(&o, 4);
     mbar_latency<<<1, 160>>>(10000, o);
+    cudaDeviceSynchronize();
+    uint8_t* src;
+    cudaMalloc(&src, 4 << 20);
+    arrive_cost<<<1, 32>>>(src, o);
     cudaDeviceSynchronize();
   }
   const size_t sm = 65536 + 32768 + 1024;

@@ -20,7 +20,7 @@ sys.path.insert(0, _ROOT)
 import paper_2407_10960_b200 as F  # noqa: E402
 
 NAMES = ["start", "producer_issued", "lut_ready", "first_stage", "seg_end", "last_seg_end", "exit",
-         "finisher_acq"]
+         "finisher_acq", "cta_barrier", "prod_policy", "prod_pdl_wait", "lut_filled", "epi_pdl_wait"]
 
 
 def main():
