@@ -613,11 +613,16 @@ def mma_fragment(a16: np.ndarray, b16: np.ndarray, c: np.ndarray) -> np.ndarray:
     return c
 
 
-def debug_times(workers: int) -> np.ndarray:
-    """Per-CTA ns timeline of the last launch (needs FLUTE_DEBUG_TIMES=1)."""
-    out = np.zeros(208 * workers, np.uint64)
+def debug_times(workers: int, slots: int = 1):
+    """Per-CTA ns timeline (diag build, FLUTE_DEBUG_TIMES=slots): for each of
+    the ring's `slots` launches, (stamps [workers][16], stage trace
+    [workers][64][3])."""
+    per = 208 * workers
+    out = np.zeros(per * slots, np.uint64)
     _check(_lib.flute_debug_times(out, workers))
-    return out[:16 * workers].reshape(workers, 16), out[16 * workers:].reshape(workers, 64, 3)
+    res = [(out[i * per:i * per + 16 * workers].reshape(workers, 16),
+            out[i * per + 16 * workers:(i + 1) * per].reshape(workers, 64, 3)) for i in range(slots)]
+    return res[0] if slots == 1 else res
 
 
 def exported_symbols() -> Sequence[str]:

@@ -42,10 +42,9 @@
 
 namespace flute_dev {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kProducerWarp = kConsumerWarps;
-constexpr int kEpilogueWarp = kConsumerWarps + 1;
-constexpr int kThreads = 32 * (kConsumerWarps + 2);
+// CW consumer warps (8 or 16; quartets of 4 warps take stages round-robin),
+// then one producer warp and one epilogue warp.
+constexpr int threads_for(int cw) { return 32 * (cw + 2); }
 constexpr int kMaxStages = 16;
 constexpr int kUnitN = 64;   // == flutesim::kUnitN (pack.hpp)
 constexpr int kUnitK = 128;  // == flutesim::kUnitK: one Stream-K unit
@@ -91,8 +90,10 @@ struct KParams {
   unsigned long long* dbg;  // per-CTA timeline (diag build, FLUTE_DEBUG_TIMES)
 };
 
-template <int BITS, int BM, int UPS>
+template <int BITS, int BM, int UPS, int CW = 8>
 struct Cfg {
+  static constexpr int kConsumerWarps = CW;
+  static constexpr int kGroups = CW / 4;  // quartets
   static constexpr int kEntries = 1 << (2 * BITS);
   static constexpr int kLutBytes = kEntries * kLutRowBytes;
   static constexpr int kSubBytes = BITS * 1024;  // 64 x 128 weights
@@ -184,10 +185,13 @@ struct Ring {
 // the NEXT launch (programmatic dependent launch) co-reside with this one, so
 // its prologue and weight prefetch overlap this launch's tail; the host keeps
 // shared memory within half an SM for those configurations.
-template <int BITS, int BM, int UPS, int OCC>
-__global__ void __launch_bounds__(kThreads, OCC)
+template <int BITS, int BM, int UPS, int OCC, int CW>
+__global__ void __launch_bounds__(threads_for(CW), OCC)
     qgemm_mma_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
-  using C = Cfg<BITS, BM, UPS>;
+  using C = Cfg<BITS, BM, UPS, CW>;
+  constexpr int kConsumerWarps = CW;
+  constexpr int kProducerWarp = CW;
+  constexpr int kEpilogueWarp = CW + 1;
   constexpr int MT = BM / 8;
   extern __shared__ __align__(1024) uint8_t smem[];
 
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
     FLUTE_STAMP(0);
     for (int s = 0; s < S; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), kConsumerWarps / 2);  // one arrive per warp of the stage's half
+      mbar_init(empty(s), 4);  // one arrive per warp of the stage's quartet
     }
     mbar_init(epi_full, kConsumerWarps);
     mbar_init(epi_empty, 1);
@@ -457,11 +461,11 @@ __global__ void __launch_bounds__(kThreads, OCC)
     if (!FLUTE_DIAG(32)) fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
     if (threadIdx.x == 0) FLUTE_STAMP(11);
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
-    // Two halves of 4 warps take alternate stages (half h: stages i with
-    // i % 2 == h), so the two warps sharing an SMSP are out of phase (one in
-    // its LUT-lookup phase while the other issues MMAs).  Warp q of a half
+    // Quartets of 4 warps take stages round-robin (quartet h: stages i with
+    // i % kGroups == h), so the warps sharing an SMSP are out of phase (one in
+    // its LUT-lookup phase while another issues MMAs).  Warp q of a quartet
     // owns k-steps 2q and 2q+1 (16 deep each) of every unit of its stages.
-    const int half = warp >> 2;
+    const int half = warp >> 2;  // this warp's quartet
     const int q4 = warp & 3;
     constexpr int KS = 2;  // k-steps per warp per unit
     // X stage = TMA box {64 k, m rows, 2*UPS chunks}, compact ([chunk][m][128 B],
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
     };
 
     int seg = 0;
-    int parity = 0;  // global stage counter & 1
+    int parity = 0;  // global stage counter % kGroups
     for (int tile = R.t_hi; uend > ubeg && tile >= R.t_lo; --tile, ++seg) {
       const int bot = R.bot(tile);
       int kt = R.top(tile);
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
       for (; kt - bot + 1 >= UPS; kt -= UPS) {
         if (parity == half) run_stage(std::integral_constant<int, UPS>{}, kt - UPS + 1, ring.s, ring.ph);
         ring.advance(S);
-        parity ^= 1;
+        if (++parity == C::kGroups) parity = 0;
       }
       if constexpr (UPS > 1) {
         const int rem = kt - bot + 1;
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
             }
           }
           ring.advance(S);
-          parity ^= 1;
+          if (++parity == C::kGroups) parity = 0;
         }
       }
       // ---- segment end: every warp parks its partial for the epilogue ----

@@ -112,17 +112,26 @@ const DevProps& props() {
 // warp 0: 64 stages x {wait begin, data ready, compute done}.
 constexpr size_t kDbgPerCta = 16 + 64 * 3;
 unsigned long long* g_dbg = nullptr;
-int g_dbg_cap = 0;
+int g_dbg_cap = 0;       // CTAs per slot
+int g_dbg_slots = 1;     // FLUTE_DEBUG_TIMES=N: ring of N launches (no per-launch memset,
+int g_dbg_next = 0;      // so programmatic-dependent launches still overlap)
 unsigned long long* debug_times_buffer(int workers) {
-  static const bool on = std::getenv("FLUTE_DEBUG_TIMES") != nullptr;
-  if (!on) return nullptr;
-  if (g_dbg_cap < workers) {
+  static const char* env = std::getenv("FLUTE_DEBUG_TIMES");
+  if (!env) return nullptr;
+  const int slots = std::max(1, std::atoi(env));
+  const size_t slot_words = static_cast<size_t>(workers) * kDbgPerCta;
+  if (g_dbg_cap < workers || g_dbg_slots != slots) {
     if (g_dbg) cudaFree(g_dbg);
-    FLUTE_CUDA(cudaMalloc(&g_dbg, static_cast<size_t>(workers) * kDbgPerCta * 8));
+    FLUTE_CUDA(cudaMalloc(&g_dbg, slot_words * slots * 8));
+    FLUTE_CUDA(cudaMemset(g_dbg, 0, slot_words * slots * 8));
     g_dbg_cap = workers;
+    g_dbg_slots = slots;
+    g_dbg_next = 0;
   }
-  FLUTE_CUDA(cudaMemset(g_dbg, 0, static_cast<size_t>(workers) * kDbgPerCta * 8));
-  return g_dbg;
+  if (slots == 1) FLUTE_CUDA(cudaMemset(g_dbg, 0, slot_words * 8));
+  unsigned long long* b = g_dbg + static_cast<size_t>(g_dbg_next) * g_dbg_cap * kDbgPerCta;
+  g_dbg_next = (g_dbg_next + 1) % slots;
+  return b;
 }
 
 int bm_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : 32; }
@@ -156,9 +165,9 @@ struct SmemPlan {
 
 // [vLUT (+ partial rows in its row gaps) | partials | barriers | stages...],
 // stage = [X (1024-aligned, zero row last) | weights | scales].
-template <int BITS, int BM, int UPS>
+template <int BITS, int BM, int UPS, int CW>
 SmemPlan plan_smem(int m, int group, int cluster, size_t cap) {
-  using Cf = Cfg<BITS, BM, UPS>;
+  using Cf = Cfg<BITS, BM, UPS, CW>;
   SmemPlan pl;
   size_t off = Cf::kLutBytes;
   pl.part_off = static_cast<uint32_t>(off);
@@ -179,16 +188,16 @@ SmemPlan plan_smem(int m, int group, int cluster, size_t cap) {
   return pl;
 }
 
-template <int BITS, int BM, int UPS, int OCC>
+template <int BITS, int BM, int UPS, int OCC, int CW>
 void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp, int cluster) {
-  using Cf = Cfg<BITS, BM, UPS>;
+  using Cf = Cfg<BITS, BM, UPS, CW>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   FLUTE_CUDA(cudaGetDevice(&dev));
-  const SmemPlan pl = plan_smem<BITS, BM, UPS>(m_rows, a.group, cluster, smem_cap(OCC));
+  const SmemPlan pl = plan_smem<BITS, BM, UPS, CW>(m_rows, a.group, cluster, smem_cap(OCC));
   if (pl.stages < 2) throw flutesim::InternalError("qgemm: shared-memory plan has < 2 stages");
-  auto kern = qgemm_mma_kernel<BITS, BM, UPS, OCC>;
+  auto kern = qgemm_mma_kernel<BITS, BM, UPS, OCC, CW>;
   if (configured_dev != dev) {
     FLUTE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem_cap(OCC))));
@@ -246,7 +255,7 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(workers));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads_for(CW));
   cfg.dynamicSmemBytes = pl.total;
   cfg.stream = static_cast<cudaStream_t>(a.stream);
   cudaLaunchAttribute attr[2];
@@ -273,13 +282,15 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 //   m <= 8 : UPS 2, OCC 2  (co-resident with the next launch)
 //   m <= 16: UPS 1, OCC 2
 //   m <= 32: UPS 2, OCC 1  (64 accumulator floats / lane: one CTA per SM)
+// (A single 16-consumer-warp CTA per SM — CW = 16, OCC = 1 — was measured
+// 10-30 % slower than two 8-warp CTAs on every configs[1] case.)
 template <int BITS>
 void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp, int cluster) {
   switch (bm_for(m_rows)) {
-    case 8: launch_impl<BITS, 8, 2, 2>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
-    case 16: launch_impl<BITS, 16, 1, 2>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
-    default: launch_impl<BITS, 32, 2, 1>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+    case 8: launch_impl<BITS, 8, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+    case 16: launch_impl<BITS, 16, 1, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+    default: launch_impl<BITS, 32, 2, 1, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
   }
 }
 
@@ -336,8 +347,13 @@ int default_workers(int m, int k, int n, int bits) {
 
 void debug_times(unsigned long long* out, int workers) {
   if (!g_dbg) throw flutesim::InputError("FLUTE_DEBUG_TIMES not enabled");
-  FLUTE_CUDA(cudaMemcpy(out, g_dbg, static_cast<size_t>(std::min(workers, g_dbg_cap)) * kDbgPerCta * 8,
-                        cudaMemcpyDeviceToHost));
+  // slot i (launch i of the ring) at out + i * workers * kDbgPerCta
+  FLUTE_CUDA(cudaDeviceSynchronize());
+  for (int i = 0; i < g_dbg_slots; ++i)
+    FLUTE_CUDA(cudaMemcpy(out + static_cast<size_t>(i) * workers * kDbgPerCta,
+                          g_dbg + static_cast<size_t>(i) * g_dbg_cap * kDbgPerCta,
+                          static_cast<size_t>(std::min(workers, g_dbg_cap)) * kDbgPerCta * 8,
+                          cudaMemcpyDeviceToHost));
 }
 
 size_t workspace_bytes(int m, int workers) {

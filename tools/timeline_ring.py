@@ -1,0 +1,66 @@
+#!/usr/bin/env python
+"""Steady-state timeline: N back-to-back launches (PDL, no sync, distinct weight
+replicas) with per-CTA stamps for each (diag build, FLUTE_DEBUG_TIMES=N ring).
+usage: python tools/timeline_ring.py M K N BITS GROUP [launches]"""
+import os
+import sys
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+L = int(sys.argv[6]) if len(sys.argv) > 6 else 6
+os.environ["FLUTE_DEBUG_TIMES"] = str(L)
+os.environ.setdefault("FLUTE_LIB", os.path.join(_ROOT, "paper_2407_10960_b200", "libflute_b200_diag.so"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+sys.path.insert(0, _ROOT)
+import paper_2407_10960_b200 as F  # noqa: E402
+
+NAMES = ["start", "producer_issued", "lut_ready", "first_stage", "seg_end", "last_seg_end", "exit",
+         "finisher_acq", "cta_barrier", "prod_policy", "prod_pdl_wait", "lut_filled", "epi_pdl_wait"]
+
+
+def main():
+    m, k, n, bits, group = (int(v) for v in sys.argv[1:6])
+    rng = np.random.default_rng(0)
+    idx, sc = F.quantize_matrix(rng.standard_normal((k, n), dtype=np.float32), bits, group)
+    dws = [F.DeviceWeights(idx, sc, F.build_nf_table(bits), bits, group) for _ in range(L)]
+    x = torch.randn(m, k, dtype=torch.float16, device="cuda")
+    y = torch.empty(m, n, dtype=torch.float16, device="cuda")
+    P = F.default_workers(m, k, n, bits)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for i in range(L):  # warm (fills the ring once)
+            dws[i].gemm(x, y, stream=st.cuda_stream)
+    st.synchronize()
+    with torch.cuda.stream(st):
+        for i in range(L):
+            dws[i].gemm(x, y, stream=st.cuda_stream)
+    st.synchronize()
+    res = F.debug_times(P, L)
+    t0 = min(int(r[0][:, 0][r[0][:, 0] > 0].min()) for r in res)
+    print(f"M={m} K={k} N={n} W{bits}g{group} P={P}, {L} back-to-back launches (us from first start)")
+    print("launch " + " ".join(f"{nm[:12]:>12s}" for nm in ["start", "prod_pdl_wait", "first_stage", "last_seg_end", "exit"]))
+    for i, (stamps, _) in enumerate(res):
+        t = stamps.astype(np.int64)
+        def col(j, f):
+            c = t[:, j]
+            c = c[c > 0]
+            return (f(c) - t0) / 1e3 if c.size else float("nan")
+        print(f"{i:6d} " + " ".join(f"{v:12.2f}" for v in
+                                    [col(0, np.min), col(10, np.median), col(3, np.median),
+                                     col(5, np.max), col(6, np.max)]))
+
+
+    if os.environ.get("STAGES"):
+        stamps, tr = res[min(3, L - 1)]
+        for cta in (0, P // 2, P - 1):
+            rows = tr[cta].astype(np.int64)
+            rows = rows[rows[:, 0] > 0]
+            print(f"  launch {min(3, L - 1)} CTA {cta}: wait_begin ready done (us; wait, compute)")
+            for i, (a, b, c) in enumerate(rows):
+                print(f"    {i:3d} {(a - t0) / 1e3:8.2f} {(b - t0) / 1e3:8.2f} {(c - t0) / 1e3:8.2f}"
+                      f"   ({(b - a) / 1e3:5.2f}, {(c - b) / 1e3:5.2f})")
+
+
+if __name__ == "__main__":
+    main()
