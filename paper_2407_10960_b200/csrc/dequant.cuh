@@ -74,8 +74,26 @@ __device__ __forceinline__ void lut_dequant4(uint32_t idx_bytes, uint32_t lane4,
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const uint32_t off = prmt(idx_bytes, lane4, 0x5504u | (static_cast<uint32_t>(p) << 4));
-    uint32_t v = lds32(lut_base + off);
+    uint32_t v = lds32_const(lut_base + off);
     const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v),
+                              (p & 1) ? __high2half2(s2) : __low2half2(s2));
+    a[p] = *reinterpret_cast<const uint32_t*>(&r);
+  }
+}
+
+// The two halves of lut_dequant4, for callers that batch the lookups of
+// several atoms ahead of their MMAs (more loads in flight per warp).
+__device__ __forceinline__ void lut_lookup4(uint32_t idx_bytes, uint32_t lane4, uint32_t lut_base,
+                                            uint32_t (&v)[4]) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+    v[p] = lds32_const(lut_base + prmt(idx_bytes, lane4, 0x5504u | (static_cast<uint32_t>(p) << 4)));
+}
+__device__ __forceinline__ void lut_scale4(const uint32_t (&v)[4], uint32_t scales, uint32_t (&a)[4]) {
+  const __half2 s2 = *reinterpret_cast<const __half2*>(&scales);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v[p]),
                               (p & 1) ? __high2half2(s2) : __low2half2(s2));
     a[p] = *reinterpret_cast<const uint32_t*>(&r);
   }

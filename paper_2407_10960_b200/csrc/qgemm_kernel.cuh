@@ -592,11 +592,15 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
       for (int r = 0; r < NS; ++r) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
+          // all 16 lookups of the k-step first, then scale + MMA per atom
+          uint32_t v[4][4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) lut_lookup4(atom_index_bytes<BITS>(lb[r][ks], j), lane4, lut, v[j]);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t scw = j == 0 ? sq[r].x : j == 1 ? sq[r].y : j == 2 ? sq[r].z : sq[r].w;
             uint32_t a[4];
-            lut_dequant4(atom_index_bytes<BITS>(lb[r][ks], j), lane4, lut, scw, a);
+            lut_scale4(v[j], scw, a);
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
               mma_16816(acc[mt][j], a, bf[r][ks][mt][0], bf[r][ks][mt][1]);

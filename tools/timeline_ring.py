@@ -32,9 +32,18 @@ def main():
         for i in range(L):  # warm (fills the ring once)
             dws[i].gemm(x, y, stream=st.cuda_stream)
     st.synchronize()
-    with torch.cuda.stream(st):
-        for i in range(L):
-            dws[i].gemm(x, y, stream=st.cuda_stream)
+    if os.environ.get("GRAPH"):  # same launches captured into a CUDA graph and replayed
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(L):
+                dws[i].gemm(x, y, stream=st.cuda_stream)
+        g.replay()
+        st.synchronize()
+        g.replay()
+    else:
+        with torch.cuda.stream(st):
+            for i in range(L):
+                dws[i].gemm(x, y, stream=st.cuda_stream)
     st.synchronize()
     res = F.debug_times(P, L)
     t0 = min(int(r[0][:, 0][r[0][:, 0] > 0].min()) for r in res)
