@@ -6,7 +6,8 @@
  *
  * Status codes mirror the reference's exception taxonomy (errors.hpp:12-50):
  *   FLUTE_OK, FLUTE_ERR_CONFIG (ConfigError), FLUTE_ERR_INPUT (InputError),
- *   FLUTE_ERR_INTERNAL (InternalError), FLUTE_ERR_CUDA (CUDA runtime/driver).
+ *   FLUTE_ERR_INTERNAL (InternalError), FLUTE_ERR_CUDA (CUDA runtime/driver),
+ *   FLUTE_ERR_OPTIMIZATION (OptimizationError, refinement only).
  * flute_last_error() returns the message of the last failure on the calling
  * thread.  Nothing here falls back to the CPU: device entry points fail with
  * FLUTE_ERR_CUDA when no sm_100 device is usable.
@@ -33,6 +34,7 @@ extern "C" {
 #define FLUTE_ERR_INPUT 2
 #define FLUTE_ERR_INTERNAL 3
 #define FLUTE_ERR_CUDA 4
+#define FLUTE_ERR_OPTIMIZATION 5
 
 const char* flute_last_error(void);
 const char* flute_version(void);
@@ -43,6 +45,9 @@ float flute_f16_to_f32(uint16_t h);
 
 /* ---- input producers (nf_table.hpp:48, quantize.hpp:45-52) --------------- */
 int flute_nf_table(int bits, float* values_out /* 2^bits */);
+/* nf_table.hpp:23-25: raw quantiles Phi^-1(p_i) (2^bits doubles) and sigma. */
+int flute_nf_quantiles(int bits, double* values_out);
+double flute_nf_sigma(void);
 int flute_quantize(const float* w /* k x n */, int k, int n, int bits, int group,
                    uint8_t* indices_out, uint16_t* scales_out);
 
@@ -153,6 +158,23 @@ int flute_weights_from_flte(const uint8_t* bytes, size_t len, void* stream, flut
 int flute_flte_write(const uint8_t* indices, const uint16_t* scales, const float* table_values,
                      int k, int n, int bits, int group, const int* layout, uint8_t* out, size_t cap,
                      size_t* len);
+
+/* ---- learned-sigma refinement --------------------
+ * flute_ste_evaluate: ste_evaluate (quantize.cpp:141-229) on the GPU.  HOST
+ * buffers: w f32 [k][n], x f32 [m][k] (calibration rows), sigma f64 [n*k/g]
+ * ([n][k/g] group order); out: *loss, grad f64 [n*k/g], idx u8 [k][n] (grad /
+ * idx may be NULL).  Indices and gradients are bit-identical to the
+ * reference; the loss equals it up to summation order.
+ * flute_refine_scales: refine_scales (quantize.cpp:231-282): `steps` descent
+ * steps at rate `lr` on the GPU; out: idx u8 [k][n], scales f16 [n][k/g]
+ * (learned factor folded in), sigma f64 [n*k/g] (may be NULL), losses[2] =
+ * {initial, final} (may be NULL).  FLUTE_ERR_OPTIMIZATION when the loss or a
+ * folded scale goes non-finite; *failed_step (may be NULL) = its step. */
+int flute_ste_evaluate(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                       const double* sigma, double* loss, double* grad, uint8_t* idx);
+int flute_refine_scales(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                        int steps, double lr, uint8_t* idx, uint16_t* scales, double* sigma,
+                        double* losses, int* failed_step);
 
 /* ---- N-column sharding ---------------------------------
  * Rank `rank` of `world` owns the 64-column tiles [rank*T/world,

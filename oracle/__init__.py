@@ -58,6 +58,47 @@ def _lay(layout) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(layout, dtype=np.int32))
 
 
+
+class RefineFailed(RuntimeError):
+    """OptimizationError of refine_scales (quantize.cpp:246-280), with its step."""
+
+    def __init__(self, step: int, what: str = ""):
+        super().__init__(f"refine_scales failed at step {step}: {what}")
+        self.step = step
+
+
+def _ste_call(fn, w, x, bits, group, sigma, chk):
+    w = np.ascontiguousarray(w, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    k, n = w.shape
+    m = x.shape[0]
+    sigma = np.ascontiguousarray(sigma, np.float64)
+    loss = C.c_double(0.0)
+    grad = np.zeros(sigma.size, np.float64)
+    idx = np.zeros((k, n), np.uint8)
+    chk(fn(w, x, m, k, n, bits, group, sigma, C.byref(loss), grad, idx), "ste_evaluate")
+    return loss.value, grad, idx
+
+
+def _refine_call(fn, w, x, bits, group, steps, lr, chk, opt_rc, err):
+    w = np.ascontiguousarray(w, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    k, n = w.shape
+    m = x.shape[0]
+    groups = k // group * n
+    idx = np.zeros((k, n), np.uint8)
+    sc = np.zeros(groups, np.uint16)
+    sigma = np.zeros(groups, np.float64)
+    losses = np.zeros(2, np.float64)
+    step = C.c_int(-1)
+    rc = fn(w, x, m, k, n, bits, group, steps, float(lr), idx, sc, sigma, losses, C.byref(step))
+    if rc == opt_rc:
+        raise RefineFailed(step.value, err())
+    chk(rc, "refine_scales")
+    return {"indices": idx, "scales": sc, "sigma": sigma, "initial_loss": float(losses[0]),
+            "final_loss": float(losses[1])}
+
+
 class Oracle:
     """The plain-C restatement (flute_oracle.c)."""
 
@@ -93,6 +134,13 @@ class Oracle:
                                        C.c_int, C.c_int, C.c_int, _u64p]
         L.orc_reference_f64.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                         _u8p, _u16p, _f32p, _f64p]
+        L.orc_nf_quantiles.argtypes = [C.c_int, _f64p]
+        L.orc_nf_sigma.restype = C.c_double
+        L.orc_ste_evaluate.argtypes = [_f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       _f64p, C.POINTER(C.c_double), _f64p, _u8p]
+        L.orc_refine_scales.argtypes = [_f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_int, C.c_double, _u8p, _u16p, _f64p, _f64p,
+                                        C.POINTER(C.c_int)]
         L.orc_reference_f64_mode.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              _u8p, _u16p, _f32p, C.c_int, _f64p]
 
@@ -116,6 +164,21 @@ class Oracle:
         out = np.zeros(1 << bits, np.float32)
         self._chk(self.lib.orc_nf_table(bits, out), "nf_table")
         return out
+
+    def nf_quantiles(self, bits: int) -> np.ndarray:
+        out = np.zeros(1 << bits, np.float64)
+        self._chk(self.lib.orc_nf_quantiles(bits, out), "nf_quantiles")
+        return out
+
+    def nf_sigma(self) -> float:
+        return float(self.lib.orc_nf_sigma())
+
+    def ste_evaluate(self, w, x, bits, group, sigma):
+        return _ste_call(self.lib.orc_ste_evaluate, w, x, bits, group, sigma, self._chk)
+
+    def refine_scales(self, w, x, bits, group, steps, lr):
+        return _refine_call(self.lib.orc_refine_scales, w, x, bits, group, steps, lr, self._chk, 4,
+                            lambda: "loss diverged")
 
     def quantize(self, w: np.ndarray, bits: int, group: int):
         w = np.ascontiguousarray(w, np.float32)
@@ -249,6 +312,11 @@ class RefLib:
         L.fref_execute.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32p,
                                    _u32p, _u32p, _u16p, _f32p, C.c_int, C.c_int, C.c_int,
                                    C.c_int, C.c_int, _u16p, _u64p]
+        L.fref_ste_evaluate.argtypes = [_f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        _f64p, C.POINTER(C.c_double), _f64p, _u8p]
+        L.fref_refine_scales.argtypes = [_f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_double, _u8p, _u16p, _f64p, _f64p,
+                                         C.POINTER(C.c_int)]
         L.fref_plan_traffic.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32p,
                                         C.c_int, C.c_int, C.c_int, C.c_int, _u64p]
 
@@ -291,6 +359,13 @@ class RefLib:
         out = np.zeros(1 << bits, np.float32)
         self._chk(self.lib.fref_nf_table(bits, out), "nf_table")
         return out
+
+    def ste_evaluate(self, w, x, bits, group, sigma):
+        return _ste_call(self.lib.fref_ste_evaluate, w, x, bits, group, sigma, self._chk)
+
+    def refine_scales(self, w, x, bits, group, steps, lr):
+        return _refine_call(self.lib.fref_refine_scales, w, x, bits, group, steps, lr, self._chk, 5,
+                            lambda: self.lib.fref_last_error().decode())
 
     def quantize(self, w: np.ndarray, bits: int, group: int):
         w = np.ascontiguousarray(w, np.float32)

@@ -112,17 +112,30 @@ double orc_inverse_normal_cdf(double p) {
   return halley(x, p);
 }
 
-int orc_nf_table(int bits, float* values_out) {
+#define ORC_NF_DELTA (0.5 * (1.0 / 30.0 + 1.0 / 32.0))
+
+/* raw NF quantiles Phi^-1(p_i) (nf_table.cpp:75-93) */
+int orc_nf_quantiles(int bits, double* q) {
   if (bits < 2 || bits > 4) return 1;
-  const double delta = 0.5 * (1.0 / 30.0 + 1.0 / 32.0);
+  const double delta = ORC_NF_DELTA;
   const int half = 1 << (bits - 1), cnt = 1 << bits;
-  double p[16], q[16];
+  double p[16];
   p[0] = delta;
   p[half - 1] = 0.5;
   p[cnt - 1] = 1.0 - delta;
   for (int i = 1; i < half - 1; ++i) p[i] = delta + (0.5 - delta) * i / (half - 1);
   for (int j = 1; j < half; ++j) p[half - 1 + j] = 0.5 + (0.5 - delta) * j / half;
   for (int i = 0; i < cnt; ++i) q[i] = orc_inverse_normal_cdf(p[i]);
+  return 0;
+}
+
+/* sigma of the NF grid (nf_table.cpp:71-73) */
+double orc_nf_sigma(void) { return 1.0 / orc_inverse_normal_cdf(1.0 - ORC_NF_DELTA); }
+
+int orc_nf_table(int bits, float* values_out) {
+  double q[16];
+  if (orc_nf_quantiles(bits, q)) return 1;
+  const int cnt = 1 << bits;
   for (int i = 0; i < cnt; ++i) values_out[i] = (float)(q[i] / q[cnt - 1]);
   for (int i = 1; i < cnt; ++i)
     if (!(values_out[i - 1] < values_out[i])) return 3;
@@ -545,4 +558,144 @@ int orc_reference_f64_mode(const uint16_t* x, int m, int k, int n, int bits, int
   }
   free(wd);
   return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Learned-sigma refinement — quantize.cpp:141-282.  Same loops, same       */
+/* binary64 operation order (compiled with -ffp-contract=off).               */
+/* ------------------------------------------------------------------------ */
+
+/* 0 ok, 1 config, 2 input (non-finite weight: *bad_i, *bad_j set) */
+static int ste_requant(const float* w, int k, int n, int bits, int group, const double* sigma,
+                       const double* q, uint8_t* idx, double* what, float* absmax) {
+  const int gpc = k / group, cnt = 1 << bits, zero_idx = (1 << (bits - 1)) - 1;
+  const long groups = (long)gpc * n;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < k; ++i) {
+      const float v = w[(size_t)i * n + j];
+      if (!isfinite(v)) return 2;
+      float* s = &absmax[(size_t)j * gpc + i / group];
+      const float a = fabsf(v);
+      if (*s < a) *s = a;
+    }
+  for (long g = 0; g < groups; ++g) {
+    const int j = (int)(g / gpc), i0 = (int)(g % gpc) * group;
+    const double eff = (double)absmax[g] * sigma[g];
+    double cand[16];
+    if (absmax[g] == 0.0f) {
+      for (int i = i0; i < i0 + group; ++i) {
+        idx[(size_t)i * n + j] = (uint8_t)zero_idx;
+        what[(size_t)i * n + j] = 0.0;
+      }
+      continue;
+    }
+    for (int c = 0; c < cnt; ++c) cand[c] = eff * q[c];
+    for (int i = i0; i < i0 + group; ++i) {
+      const double u = (double)w[(size_t)i * n + j];
+      int best = 0;
+      double bd = fabs(cand[0] - u);
+      for (int c = 1; c < cnt; ++c) {
+        const double d = fabs(cand[c] - u);
+        if (d < bd) { bd = d; best = c; }
+      }
+      idx[(size_t)i * n + j] = (uint8_t)best;
+      what[(size_t)i * n + j] = cand[best];
+    }
+  }
+  return 0;
+}
+
+int orc_ste_evaluate(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                     const double* sigma, double* loss, double* grad, uint8_t* idx) {
+  if (!cfg_ok(bits, group, k)) return 1;
+  double q[16];
+  orc_nf_quantiles(bits, q);
+  const int gpc = k / group;
+  const long groups = (long)gpc * n;
+  float* absmax = (float*)calloc((size_t)groups, sizeof(float));
+  double* what = (double*)malloc(sizeof(double) * (size_t)k * n);
+  double* err = (double*)malloc(sizeof(double) * (size_t)m * n);
+  int rc = ste_requant(w, k, n, bits, group, sigma, q, idx, what, absmax);
+  if (rc == 0) {
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < m; ++t)
+      for (int j = 0; j < n; ++j) {
+        double acc = 0.0;
+        for (int i = 0; i < k; ++i)
+          acc += (double)x[(size_t)t * k + i] * (what[(size_t)i * n + j] - (double)w[(size_t)i * n + j]);
+        err[(size_t)t * n + j] = acc;
+      }
+    double l = 0.0;
+    for (long e = 0; e < (long)m * n; ++e) l += err[e] * err[e];
+    *loss = l;
+#pragma omp parallel for schedule(static)
+    for (long g = 0; g < groups; ++g) {
+      const int j = (int)(g / gpc), i0 = (int)(g % gpc) * group;
+      double acc = 0.0;
+      if (absmax[g] != 0.0f) {
+        for (int i = i0; i < i0 + group; ++i) {
+          double gij = 0.0;
+          for (int t = 0; t < m; ++t) gij += (double)x[(size_t)t * k + i] * err[(size_t)t * n + j];
+          acc += 2.0 * gij * (double)absmax[g] * q[idx[(size_t)i * n + j]];
+        }
+      }
+      grad[g] = acc;
+    }
+  }
+  free(absmax);
+  free(what);
+  free(err);
+  return rc;
+}
+
+/* 0 ok, 1 config, 2 input, 4 optimization error (*failed_step set) */
+int orc_refine_scales(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                      int steps, double lr, uint8_t* idx, uint16_t* scales, double* sigma_out,
+                      double* losses, int* failed_step) {
+  if (steps < 0) return 2;
+  int rc = orc_quantize(w, k, n, bits, group, idx, scales);
+  if (rc) return rc;
+  const long groups = (long)(k / group) * n;
+  const double sigma0 = orc_nf_sigma();
+  double* sig = sigma_out;
+  double* grad = (double*)malloc(sizeof(double) * (size_t)groups);
+  uint8_t* tmp = (uint8_t*)malloc((size_t)k * n);
+  for (long g = 0; g < groups; ++g) sig[g] = sigma0;
+  double l = 0.0;
+  if (steps == 0) {
+    orc_ste_evaluate(w, x, m, k, n, bits, group, sig, &l, grad, tmp);
+    losses[0] = losses[1] = l;
+    free(grad);
+    free(tmp);
+    return 0;
+  }
+  for (int step = 0; step < steps; ++step) {
+    orc_ste_evaluate(w, x, m, k, n, bits, group, sig, &l, grad, tmp);
+    if (!isfinite(l)) { *failed_step = step; rc = 4; goto done; }
+    if (step == 0) losses[0] = l;
+    for (long g = 0; g < groups; ++g) sig[g] -= lr * grad[g];
+  }
+  orc_ste_evaluate(w, x, m, k, n, bits, group, sig, &l, grad, idx);
+  if (!isfinite(l)) { *failed_step = steps; rc = 4; goto done; }
+  losses[1] = l;
+  {
+    const int gpc = k / group;
+    for (long g = 0; g < groups; ++g) {
+      const int j = (int)(g / gpc), i0 = (int)(g % gpc) * group;
+      float am = 0.0f;
+      for (int i = i0; i < i0 + group; ++i) {
+        const float a = fabsf(w[(size_t)i * n + j]);
+        if (am < a) am = a;
+      }
+      const double folded = (double)am * sig[g] / sigma0;
+      if (!(folded >= 0.0) || !isfinite(folded)) { *failed_step = steps; rc = 4; goto done; }
+      const uint16_t h = orc_f32_to_f16((float)folded);
+      if ((h & 0x7C00u) == 0x7C00u) { *failed_step = steps; rc = 4; goto done; }
+      scales[g] = h;
+    }
+  }
+done:
+  free(grad);
+  free(tmp);
+  return rc;
 }

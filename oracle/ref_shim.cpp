@@ -309,4 +309,44 @@ int fref_plan_traffic(int m, int k, int n, int bits, int group, const int* layou
   });
 }
 
+// Learned-sigma refinement (quantize.cpp:141-282).  w: k x n, x: m x k
+// row-major f32; sigma/grad [n][k/g] f64.  5 = OptimizationError (*step set).
+int fref_ste_evaluate(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                      const double* sigma, double* loss, double* grad, std::uint8_t* idx) {
+  return guarded([&] {
+    MatF W(k, n), X(m, k);
+    std::memcpy(W.data.data(), w, sizeof(float) * static_cast<std::size_t>(k) * n);
+    std::memcpy(X.data.data(), x, sizeof(float) * static_cast<std::size_t>(m) * k);
+    const std::size_t groups = static_cast<std::size_t>(k / group) * n;
+    const SteEval e = ste_evaluate(W, X, QuantConfig{bits, group},
+                                   std::span<const double>(sigma, groups));
+    *loss = e.loss;
+    std::memcpy(grad, e.grad.data(), groups * sizeof(double));
+    std::memcpy(idx, e.indices.data(), e.indices.size());
+  });
+}
+
+int fref_refine_scales(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                       int steps, double lr, std::uint8_t* idx, std::uint16_t* scales,
+                       double* sigma, double* losses, int* step) {
+  try {
+    MatF W(k, n), X(m, k);
+    std::memcpy(W.data.data(), w, sizeof(float) * static_cast<std::size_t>(k) * n);
+    std::memcpy(X.data.data(), x, sizeof(float) * static_cast<std::size_t>(m) * k);
+    const RefineResult r = refine_scales(W, X, QuantConfig{bits, group}, steps, lr);
+    std::memcpy(idx, r.quantized.indices.data(), r.quantized.indices.size());
+    for (std::size_t g = 0; g < r.quantized.scales.size(); ++g) scales[g] = r.quantized.scales[g].to_bits();
+    std::memcpy(sigma, r.sigma_tilde.data(), r.sigma_tilde.size() * sizeof(double));
+    losses[0] = r.initial_loss;
+    losses[1] = r.final_loss;
+    return 0;
+  } catch (const OptimizationError& e) {
+    g_err = e.what();
+    *step = e.step;
+    return 5;
+  } catch (...) {
+    return guarded([] { throw; });
+  }
+}
+
 }  // extern "C"

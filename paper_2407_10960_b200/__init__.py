@@ -47,7 +47,14 @@ class CudaError(FluteError):
     code = 4
 
 
-_ERRS = {1: ConfigError, 2: InputError, 3: InternalError, 4: CudaError}
+class OptimizationError(FluteError):
+    """refine_scales' loss or folded scale went non-finite (errors.hpp
+    OptimizationError); .step is the failing step."""
+    code = 5
+    step = -1
+
+
+_ERRS = {1: ConfigError, 2: InputError, 3: InternalError, 4: CudaError, 5: OptimizationError}
 
 
 def build(force: bool = False) -> str:
@@ -75,6 +82,7 @@ _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
 
 # Every symbol include/flute_c.h declares, with its ctypes signature.
@@ -84,6 +92,8 @@ _SIGS = {
     "flute_f32_to_f16": (C.c_uint16, [C.c_float]),
     "flute_f16_to_f32": (C.c_float, [C.c_uint16]),
     "flute_nf_table": (C.c_int, [C.c_int, _f32p]),
+    "flute_nf_quantiles": (C.c_int, [C.c_int, _f64p]),
+    "flute_nf_sigma": (C.c_double, []),
     "flute_quantize": (C.c_int, [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _u16p]),
     "flute_canonical_words": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "flute_pack_canonical": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, _i32p, _u32p, _vp]),
@@ -133,6 +143,11 @@ _SIGS = {
     "flute_weights_from_flte": (C.c_int, [_u8p, C.c_size_t, _vp, C.POINTER(_vp)]),
     "flute_flte_write": (C.c_int, [_u8p, _u16p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, _i32p,
                                    _vp, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "flute_ste_evaluate": (C.c_int, [_f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     _f64p, C.POINTER(C.c_double), _f64p, _u8p]),
+    "flute_refine_scales": (C.c_int, [_f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.c_int, C.c_double, _u8p, _u16p, _f64p, _f64p,
+                                      C.POINTER(C.c_int)]),
     "flute_shard_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(C.c_int), C.POINTER(C.c_int),
                                     C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
@@ -548,6 +563,69 @@ def quantize_matrix_device(w, bits: int, group: int, stream=None):
     _check(_lib.flute_quantize_device(w.data_ptr(), k, n, bits, group, idx.data_ptr(),
                                       sc.data_ptr(), _stream_ptr(stream)))
     return idx, sc
+
+
+def nf_quantiles(bits: int) -> np.ndarray:
+    """nf_table.hpp nf_quantiles(bits): raw Phi^-1(p_i), binary64."""
+    out = np.zeros(1 << bits, np.float64)
+    _check(_lib.flute_nf_quantiles(bits, out))
+    return out
+
+
+def nf_sigma() -> float:
+    """nf_table.hpp nf_sigma(): 1 / Phi^-1(1 - delta)."""
+    return float(_lib.flute_nf_sigma())
+
+
+def _calib_pair(w, x_calib):
+    w = np.ascontiguousarray(w, np.float32)
+    x = np.ascontiguousarray(x_calib, np.float32)
+    if w.ndim != 2 or x.ndim != 2:
+        raise InputError("w and x_calib must be 2-D")
+    if x.shape[1] != w.shape[0]:  # quantize.cpp:145-150
+        raise InputError(f"calibration matrix has {x.shape[1]} columns, weights have "
+                         f"{w.shape[0]} rows")
+    return w, x
+
+
+def ste_evaluate(w: np.ndarray, x_calib: np.ndarray, bits: int, group: int, sigma_tilde):
+    """quantize.hpp ste_evaluate on the GPU: (loss, grad f64 [n*k/g], indices
+    u8 [k][n]).  w f32 [k][n], x_calib f32 [m][k], sigma_tilde [n*k/g]."""
+    w, x = _calib_pair(w, x_calib)
+    k, n = w.shape
+    sigma = np.ascontiguousarray(sigma_tilde, np.float64)
+    if group > 0 and sigma.size != k // group * n:  # quantize.cpp:155-157
+        raise InputError("sigma_tilde has wrong group count")
+    loss = C.c_double(0.0)
+    grad = np.zeros(sigma.size, np.float64)
+    idx = np.zeros((k, n), np.uint8)
+    _check(_lib.flute_ste_evaluate(w, x, x.shape[0], k, n, bits, group, sigma, C.byref(loss),
+                                   grad, idx))
+    return loss.value, grad, idx
+
+
+def refine_scales(w: np.ndarray, x_calib: np.ndarray, bits: int, group: int, steps: int,
+                  lr: float) -> dict:
+    """quantize.hpp refine_scales on the GPU: {indices, scales (binary16 bits,
+    learned factor folded in), sigma, initial_loss, final_loss}; raises
+    OptimizationError (with .step) like the reference."""
+    w, x = _calib_pair(w, x_calib)
+    k, n = w.shape
+    groups = k // max(group, 1) * n
+    idx = np.zeros((k, n), np.uint8)
+    sc = np.zeros(groups, np.uint16)
+    sigma = np.zeros(groups, np.float64)
+    losses = np.zeros(2, np.float64)
+    step = C.c_int(-1)
+    rc = _lib.flute_refine_scales(w, x, x.shape[0], k, n, bits, group, steps, float(lr), idx, sc,
+                                  sigma, losses, C.byref(step))
+    if rc == OptimizationError.code:
+        e = OptimizationError(_lib.flute_last_error().decode())
+        e.step = step.value
+        raise e
+    _check(rc)
+    return {"indices": idx, "scales": sc, "sigma": sigma, "initial_loss": float(losses[0]),
+            "final_loss": float(losses[1])}
 
 
 def flte_write(indices: np.ndarray, scales: np.ndarray, table_values: np.ndarray, bits: int,

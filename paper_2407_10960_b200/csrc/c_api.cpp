@@ -13,6 +13,7 @@
 #include "flutesim/flte.hpp"
 #include "flutesim/errors.hpp"
 #include "flutesim/mma.hpp"
+#include "flutesim/quantize.hpp"
 
 using namespace flutesim;
 
@@ -38,6 +39,9 @@ int guard(F&& f) {
   } catch (const InternalError& e) {
     g_last_error = e.what();
     return FLUTE_ERR_INTERNAL;
+  } catch (const OptimizationError& e) {
+    g_last_error = e.what();
+    return FLUTE_ERR_OPTIMIZATION;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return FLUTE_ERR_INTERNAL;
@@ -109,6 +113,16 @@ int flute_nf_table(int bits, float* values_out) {
     std::memcpy(values_out, t.values.data(), t.values.size() * sizeof(float));
   });
 }
+
+int flute_nf_quantiles(int bits, double* values_out) {
+  return guard([&] {
+    need(values_out, "values_out");
+    const std::vector<double> q = nf_quantiles(bits);
+    std::memcpy(values_out, q.data(), q.size() * sizeof(double));
+  });
+}
+
+double flute_nf_sigma(void) { return nf_sigma(); }
 
 int flute_quantize(const float* w, int k, int n, int bits, int group, uint8_t* indices_out,
                    uint16_t* scales_out) {
@@ -438,6 +452,59 @@ int flute_weights_from_device(const uint8_t* idx_dev, const uint16_t* scales_dev
     *out = wrap(DeviceWeights::from_device_indices(idx_dev, scales_dev, t, k, n, QuantConfig{bits, group},
                                                    stream),
                 k, n, bits, group);
+  });
+}
+
+namespace {
+MatF host_matrix(const float* p, int rows, int cols, const char* what) {
+  need(p, what);
+  if (rows < 1 || cols < 1) throw ConfigError(std::string(what) + ": dimensions must be positive");
+  MatF m(rows, cols);
+  std::memcpy(m.data.data(), p, static_cast<std::size_t>(rows) * cols * sizeof(float));
+  return m;
+}
+}  // namespace
+
+int flute_ste_evaluate(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                       const double* sigma, double* loss, double* grad, uint8_t* idx) {
+  return guard([&] {
+    need(sigma, "sigma");
+    need(loss, "loss");
+    const MatF W = host_matrix(w, k, n, "w");
+    const MatF X = host_matrix(x, m, k, "x");
+    const QuantConfig cfg{bits, group};
+    cfg.validate(k);
+    const std::size_t groups = static_cast<std::size_t>(k / group) * n;
+    const SteEval e = ste_evaluate(W, X, cfg, std::span<const double>(sigma, groups));
+    *loss = e.loss;
+    if (grad) std::memcpy(grad, e.grad.data(), groups * sizeof(double));
+    if (idx) std::memcpy(idx, e.indices.data(), e.indices.size());
+  });
+}
+
+int flute_refine_scales(const float* w, const float* x, int m, int k, int n, int bits, int group,
+                        int steps, double lr, uint8_t* idx, uint16_t* scales, double* sigma,
+                        double* losses, int* failed_step) {
+  if (failed_step) *failed_step = -1;
+  return guard([&] {
+    need(idx, "idx");
+    need(scales, "scales");
+    const MatF W = host_matrix(w, k, n, "w");
+    const MatF X = host_matrix(x, m, k, "x");
+    RefineResult r;
+    try {
+      r = refine_scales(W, X, QuantConfig{bits, group}, steps, lr);
+    } catch (const OptimizationError& e) {
+      if (failed_step) *failed_step = e.step;
+      throw;
+    }
+    std::memcpy(idx, r.quantized.indices.data(), r.quantized.indices.size());
+    for (std::size_t g = 0; g < r.quantized.scales.size(); ++g) scales[g] = r.quantized.scales[g].bits;
+    if (sigma) std::memcpy(sigma, r.sigma_tilde.data(), r.sigma_tilde.size() * sizeof(double));
+    if (losses) {
+      losses[0] = r.initial_loss;
+      losses[1] = r.final_loss;
+    }
   });
 }
 

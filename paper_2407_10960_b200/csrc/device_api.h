@@ -79,6 +79,39 @@ void pack_device_on_device(const std::uint8_t* idx, int k, int n, int bits, int 
 void scales_device_on_device(const std::uint16_t* sc, int k, int n, int group,
                              std::uint16_t* out, void* stream);
 
+// Learned-sigma refinement state (refine_kernels.cu): W f32 [k][n] and X f32
+// [m][k] uploaded once; evaluate() runs one straight-through evaluation at the
+// device sigma and returns the loss; descend() applies sigma -= lr * grad.
+class SteDevice {
+ public:
+  SteDevice(const float* w_host, const float* x_host, int m, int k, int n, int group,
+            const std::vector<double>& quantiles);
+  ~SteDevice();
+  SteDevice(const SteDevice&) = delete;
+  SteDevice& operator=(const SteDevice&) = delete;
+  void set_sigma(const double* sigma_host);
+  double evaluate();
+  void descend(double lr);
+  // any pointer may be null
+  void get(double* sigma, double* grad, std::uint8_t* idx, float* absmax) const;
+  long groups() const { return groups_; }
+
+ private:
+  int m_, k_, n_, group_, nq_;
+  long groups_ = 0;
+  float* w_ = nullptr;
+  float* x_ = nullptr;
+  double* q_ = nullptr;
+  double* sigma_ = nullptr;
+  double* grad_ = nullptr;
+  float* absmax_ = nullptr;
+  std::uint8_t* idx_ = nullptr;
+  double* d_ = nullptr;
+  double* e_ = nullptr;
+  double* scalars_ = nullptr;
+  unsigned long long* bad_ = nullptr;
+};
+
 // Small RAII device buffer helpers used by the host layer.
 void* dev_alloc(std::size_t bytes);
 void dev_free(void* p);

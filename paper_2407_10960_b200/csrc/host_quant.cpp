@@ -140,8 +140,12 @@ QuantizedMatrix quantize_matrix(const MatF& w, const QuantConfig& cfg) {
     for (int j = 0; j < n; ++j) {
       const float v = w(i, j);
       if (!std::isfinite(v)) {
-        throw InputError("quantize: non-finite weight at (" + std::to_string(i) + ", " +
-                         std::to_string(j) + ")");
+        // report the first hit of the reference's j-major scan (quantize.cpp:44-63)
+        for (int jj = 0; jj < n; ++jj)
+          for (int ii = 0; ii < k; ++ii)
+            if (!std::isfinite(w(ii, jj)))
+              throw InputError("quantize: non-finite weight at (" + std::to_string(ii) + ", " +
+                               std::to_string(jj) + ")");
       }
       float& s = absmax[static_cast<std::size_t>(j) * gpc + i / g];
       s = std::max(s, std::abs(v));
