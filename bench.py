@@ -292,9 +292,10 @@ def run_ours(args):
                     torch.matmul(xs[(m, k)], wd[r % REPLICAS], out=ys[(m, n)])
             res = {}
             for name, gr in (("ours", gcase), ("cublas_fp16", gcb)):
-                for _ in range(3):
-                    gr.replay()
-                stream.synchronize()
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        gr.replay()
+                torch.cuda.synchronize()  # warm replays must not spill into the timed ones
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 with torch.cuda.stream(stream):
                     e0.record()
@@ -311,9 +312,10 @@ def run_ours(args):
                              "speedup_vs_cublas": round(res["cublas_fp16"] / res["ours"], 2)})
 
     # ---- timed region ----
-    for _ in range(reps_warm):
-        graph.replay()
-    stream.synchronize()
+    with torch.cuda.stream(stream):
+        for _ in range(reps_warm):
+            graph.replay()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -27,12 +27,14 @@ def timeit(fn, reps):
         e0.record(); fn(); e1.record()
     e1.synchronize()
     return e0.elapsed_time(e1) * 1e3 / reps
-L = 4 * R
+L = int(os.environ.get("GL", "4")) * R
 eager = timeit(lambda: run(L), L)
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g, stream=st):
     run(L)
-g.replay(); st.synchronize()
+with torch.cuda.stream(st):
+    g.replay()
+torch.cuda.synchronize()  # the warm replay must not overlap the timed ones
 graph = timeit(lambda: [g.replay() for _ in range(5)], 5 * L)
 b = F.algorithmic_bytes(m, k, n, bits, group)
 print(f"M={m} K={k} N={n} W{bits}g{group} R={R} workers={W or 'default'} pdl={'off' if os.environ.get('FLUTE_NO_PDL') else 'on'}: "

@@ -22,8 +22,9 @@ def gtime(fn, reps=20):
     with torch.cuda.graph(g, stream=st):
         for _ in range(reps):
             fn()
-    g.replay()
-    st.synchronize()
+    with torch.cuda.stream(st):
+        g.replay()
+    torch.cuda.synchronize()  # the warm replay must not overlap the timed ones
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     with torch.cuda.stream(st):
         e0.record()

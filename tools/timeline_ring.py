@@ -39,7 +39,13 @@ def main():
                 dws[i].gemm(x, y, stream=st.cuda_stream)
         g.replay()
         st.synchronize()
-        g.replay()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        with torch.cuda.stream(st):
+            e0.record()
+            g.replay()
+            e1.record()
+        e1.synchronize()
+        print(f"events around one replay: {e0.elapsed_time(e1) * 1e3 / L:.2f} us per launch")
     else:
         with torch.cuda.stream(st):
             for i in range(L):
@@ -59,6 +65,14 @@ def main():
                                     [col(0, np.min), col(10, np.median), col(3, np.median),
                                      col(5, np.max), col(6, np.max)]))
 
+
+    exits = []
+    for stamps, _ in res:
+        c = stamps.astype(np.int64)[:, 6]
+        exits.append(c[c > 0].max())
+    if L > 3:
+        print(f"steady state: {(exits[-1] - exits[1]) / (L - 2) / 1e3:.2f} us per launch "
+              f"(last-CTA exit to last-CTA exit, launches 1..{L - 1})")
 
     if os.environ.get("STAGES"):
         stamps, tr = res[min(3, L - 1)]
