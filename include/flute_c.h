@@ -136,6 +136,12 @@ int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int work
 /* End-to-end: x and y are HOST pointers; copies in, GEMM, copies out, syncs. */
 int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
                     int workers, void* stream);
+/* A batch of `count` end-to-end GEMMs (handle ws[i], host x_host[i] [m[i]][k_i]
+ * -> host y_host[i] [m[i]][n_i]; a handle may repeat).  Input copies, GEMMs (on
+ * `stream`) and output copies are pipelined over three streams; returns when
+ * every output is in host memory.  Pinned host buffers make the copies DMA. */
+int flute_gemm_host_batch(flute_weights* const* ws, const uint16_t* const* x_host, const int* m,
+                          uint16_t* const* y_host, int count, int workers, void* stream);
 
 /* ---- weight preparation on the device / FLTE ----------
  * flute_quantize_device: quantize_matrix (quantize.cpp:81-128) on the GPU for

@@ -159,6 +159,12 @@ class DeviceWeights {
   // Raw host buffers (f16 bits; pinned memory makes the copies truly async).
   void gemm_host_raw(const std::uint16_t* x_host, int m, std::uint16_t* y_host, int workers = 0,
                      void* stream = nullptr);
+  // A batch of GEMMs on host buffers (one per handle; a handle may repeat):
+  // input copies, GEMMs and output copies pipelined across three streams
+  // (GEMMs on `stream`); returns when every y_host[i] holds its result.
+  static void gemm_host_batch(DeviceWeights* const* ws, const std::uint16_t* const* x_host,
+                              const int* m, std::uint16_t* const* y_host, int count,
+                              int workers = 0, void* stream = nullptr);
 
   struct Impl;
 

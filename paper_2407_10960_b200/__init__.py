@@ -132,6 +132,8 @@ _SIGS = {
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "flute_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _vp]),
     "flute_gemm_host": (C.c_int, [_vp, _u16p, C.c_int, _u16p, C.c_int, _vp]),
+    "flute_gemm_host_batch": (C.c_int, [C.POINTER(_vp), C.POINTER(C.c_void_p), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_void_p), C.c_int, C.c_int, _vp]),
     "flute_execute": (C.c_int, [_u16p, C.c_int, _u32p, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                 _i32p, _u16p, _u32p, C.c_int, C.c_int, C.c_int, C.c_int, _u16p,
                                 _u64p]),
@@ -547,6 +549,32 @@ def execute(x16: np.ndarray, slices, k: int, n: int, bits: int, group: int, scal
                               np.ascontiguousarray(vlut_words, np.uint32), dup, workers, stages,
                               tile_m, y, st))
     return MatmulResult(y, dict(zip(TRAFFIC_FIELDS, (int(v) for v in st))))
+
+
+def gemm_host_batch(items, workers: int = 0, stream=None) -> None:
+    """End-to-end batch (flute_gemm_host_batch): items = [(DeviceWeights,
+    x16 uint16 [m][k] host array, out uint16 [m][n] host array), ...].  Input
+    copies, GEMMs and output copies are pipelined; returns when every out is
+    filled.  Use page-locked arrays for DMA copies."""
+    cnt = len(items)
+    hs = (_vp * cnt)()
+    xs = (C.c_void_p * cnt)()
+    ys = (C.c_void_p * cnt)()
+    ms = (C.c_int * cnt)()
+    keep = []
+    for i, (dw, x16, out) in enumerate(items):
+        x16 = np.ascontiguousarray(x16, np.uint16)
+        if x16.ndim != 2 or x16.shape[1] != dw.k:
+            raise InputError(f"item {i}: x must be uint16 [m][{dw.k}]")
+        if (out.dtype != np.uint16 or out.shape != (x16.shape[0], dw.n)
+                or not out.flags.c_contiguous):
+            raise InputError(f"item {i}: out must be a C-contiguous uint16 [m][{dw.n}] array")
+        keep.append(x16)
+        hs[i] = dw._h
+        xs[i] = x16.ctypes.data
+        ys[i] = out.ctypes.data
+        ms[i] = x16.shape[0]
+    _check(_lib.flute_gemm_host_batch(hs, xs, ms, ys, cnt, workers, _stream_ptr(stream)))
 
 
 def quantize_matrix_device(w, bits: int, group: int, stream=None):

@@ -598,6 +598,24 @@ int flute_gemm(flute_weights* w, const void* x_dev, int m, void* y_dev, int work
   });
 }
 
+int flute_gemm_host_batch(flute_weights* const* ws, const uint16_t* const* x_host, const int* m,
+                          uint16_t* const* y_host, int count, int workers, void* stream) {
+  return guard([&] {
+    if (count > 0) {
+      need(ws, "weights");
+      need(x_host, "x_host");
+      need(m, "m");
+      need(y_host, "y_host");
+    }
+    std::vector<DeviceWeights*> h(static_cast<std::size_t>(std::max(count, 0)));
+    for (int i = 0; i < count; ++i) {
+      need(ws[i], "weights[i]");
+      h[i] = ws[i]->impl;
+    }
+    DeviceWeights::gemm_host_batch(h.data(), x_host, m, y_host, count, workers, stream);
+  });
+}
+
 int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
                     int workers, void* stream) {
   return guard([&] {

@@ -112,6 +112,19 @@ class SteDevice {
   unsigned long long* bad_ = nullptr;
 };
 
+// A batch of GEMMs on host buffers (host_batch, qgemm_mma.cu): H2D of every
+// input on an internal copy stream, item i's GEMM on `stream` once its input
+// has landed, D2H of its output on a second copy stream; returns when every
+// output is in host memory.  gemm(x_dev, y_dev, stream) enqueues one GEMM.
+struct HostBatchItem {
+  std::function<void(const void*, void*, void*)> gemm;
+  const void* x_host = nullptr;
+  std::size_t x_bytes = 0;
+  void* y_host = nullptr;
+  std::size_t y_bytes = 0;
+};
+void host_batch(const std::vector<HostBatchItem>& items, void* stream);
+
 // Small RAII device buffer helpers used by the host layer.
 void* dev_alloc(std::size_t bytes);
 void dev_free(void* p);

@@ -365,6 +365,28 @@ void DeviceWeights::gemm_host_raw(const std::uint16_t* x_host, int m, std::uint1
   flute_dev::stream_sync(stream);
 }
 
+void DeviceWeights::gemm_host_batch(DeviceWeights* const* ws, const std::uint16_t* const* x_host,
+                                    const int* m, std::uint16_t* const* y_host, int count,
+                                    int workers, void* stream) {
+  if (count < 0) throw ConfigError("gemm_host_batch: count must be >= 0");
+  std::vector<flute_dev::HostBatchItem> items(static_cast<std::size_t>(count));
+  for (int i = 0; i < count; ++i) {
+    if (ws[i] == nullptr || x_host[i] == nullptr || y_host[i] == nullptr)
+      throw InputError("gemm_host_batch: null handle or buffer at item " + std::to_string(i));
+    if (m[i] < 1) throw ConfigError("gemm_host_batch: m must be >= 1");
+    Impl* im = ws[i]->impl_.get();
+    const int mi = m[i];
+    items[i].gemm = [im, mi, workers](const void* x, void* y, void* st) {
+      im->gemm(x, mi, y, workers, st);
+    };
+    items[i].x_host = x_host[i];
+    items[i].x_bytes = static_cast<std::size_t>(mi) * im->k * 2;
+    items[i].y_host = y_host[i];
+    items[i].y_bytes = static_cast<std::size_t>(mi) * im->n * 2;
+  }
+  flute_dev::host_batch(items, stream);
+}
+
 // ---------------------------------------------------------------------------
 // Reference API
 // ---------------------------------------------------------------------------

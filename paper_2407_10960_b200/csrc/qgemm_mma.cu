@@ -644,4 +644,94 @@ void dev_zero(void* p, size_t bytes, void* stream) {
 }
 void stream_sync(void* stream) { FLUTE_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); }
 
+// ---------------------------------------------------------------------------
+// host-buffer batches: copies in on one stream, GEMMs on the caller's stream,
+// copies out on a third, chained by events, so item i's H2D and item i-1's
+// D2H overlap the GEMMs.  Staging comes from a per-thread, per-device arena.
+// ---------------------------------------------------------------------------
+
+namespace {
+struct BatchCtx {
+  int dev = -1;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> in_ready, out_ready;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+
+  void init(int d) {
+    dev = d;
+    FLUTE_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    FLUTE_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  }
+  void events(size_t count) {
+    while (in_ready.size() < count) {
+      cudaEvent_t a, b;
+      FLUTE_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      FLUTE_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      in_ready.push_back(a);
+      out_ready.push_back(b);
+    }
+  }
+  void* staging(size_t bytes) {
+    if (bytes > arena_bytes) {
+      if (arena) FLUTE_CUDA(cudaFree(arena));
+      arena = nullptr;
+      FLUTE_CUDA(cudaMalloc(&arena, bytes));
+      arena_bytes = bytes;
+    }
+    return arena;
+  }
+};
+}  // namespace
+
+void host_batch(const std::vector<HostBatchItem>& items, void* stream) {
+  if (items.empty()) return;
+  static thread_local std::vector<BatchCtx> ctxs;
+  int dev = 0;
+  FLUTE_CUDA(cudaGetDevice(&dev));
+  if (static_cast<int>(ctxs.size()) <= dev) ctxs.resize(dev + 1);
+  BatchCtx& c = ctxs[dev];
+  if (c.dev < 0) c.init(dev);
+  c.events(items.size());
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<size_t> xo(items.size()), yo(items.size());
+  size_t total = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    xo[i] = total;
+    total += (items[i].x_bytes + 255) / 256 * 256;
+    yo[i] = total;
+    total += (items[i].y_bytes + 255) / 256 * 256;
+  }
+  uint8_t* base = static_cast<uint8_t*>(c.staging(total));
+  // copies in: ordered after whatever the caller queued on its stream
+  cudaEvent_t start = c.out_ready[0];
+  FLUTE_CUDA(cudaEventRecord(start, st));
+  FLUTE_CUDA(cudaStreamWaitEvent(c.h2d, start, 0));
+  for (size_t i = 0; i < items.size(); ++i) {
+    FLUTE_CUDA(cudaMemcpyAsync(base + xo[i], items[i].x_host, items[i].x_bytes,
+                               cudaMemcpyHostToDevice, c.h2d));
+    FLUTE_CUDA(cudaEventRecord(c.in_ready[i], c.h2d));
+  }
+  try {
+    for (size_t i = 0; i < items.size(); ++i) {
+      // an input already resident needs no wait node (keeps consecutive GEMMs
+      // adjacent for programmatic dependent launch)
+      if (cudaEventQuery(c.in_ready[i]) != cudaSuccess)
+        FLUTE_CUDA(cudaStreamWaitEvent(st, c.in_ready[i], 0));
+      items[i].gemm(base + xo[i], base + yo[i], stream);
+      FLUTE_CUDA(cudaEventRecord(c.out_ready[i], st));
+      FLUTE_CUDA(cudaStreamWaitEvent(c.d2h, c.out_ready[i], 0));
+      FLUTE_CUDA(cudaMemcpyAsync(items[i].y_host, base + yo[i], items[i].y_bytes,
+                                 cudaMemcpyDeviceToHost, c.d2h));
+    }
+  } catch (...) {
+    // drain what was queued before the failure so the arena is free again
+    cudaStreamSynchronize(c.h2d);
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(c.d2h);
+    throw;
+  }
+  FLUTE_CUDA(cudaStreamSynchronize(c.d2h));
+}
+
 }  // namespace flute_dev

@@ -316,13 +316,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // y[m][n] = f16(sum_z part[z][m][n]), z ascending (deterministic).
-__global__ void splitk_reduce_kernel(const float* __restrict__ part, __half* __restrict__ y, int splits,
+// Sums the split partials in fixed split order and re-zeroes them: the
+// workspace is shared with the Stream-K path, whose slots must read zero
+// ("unwritten") at rest (qgemm_kernel.cuh fixup protocol).
+__global__ void splitk_reduce_kernel(float* __restrict__ part, __half* __restrict__ y, int splits,
                                      size_t mn) {
   pdl_wait();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < mn;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float acc = part[i];
-    for (int z = 1; z < splits; ++z) acc += part[static_cast<size_t>(z) * mn + i];
+    part[i] = 0.f;
+    for (int z = 1; z < splits; ++z) {
+      acc += part[static_cast<size_t>(z) * mn + i];
+      part[static_cast<size_t>(z) * mn + i] = 0.f;
+    }
     y[i] = __float2half_rn(acc);
   }
 }

@@ -356,3 +356,46 @@ def test_autotune_keeps_results_in_bound(F, orc, gpu):
     assert _within(y1, orc.reference_f64(x16, idx, bits, group, scales, table))[0]
     with pytest.raises(F.ConfigError):
         dw.autotune(64)
+
+
+def test_gemm_host_batch_matches_device_path(F, gpu):
+    """flute_gemm_host_batch (pipelined host-buffer batch, bench.py's e2e path)
+    returns, item for item, the bits of the device-resident gemm(); a handle
+    may repeat inside one batch."""
+    torch = gpu
+    rng = np.random.default_rng(42)
+    shapes = [(256, 320, 3), (512, 128, 4), (384, 192, 2)]
+    hs = []
+    for (k, n, bits) in shapes:
+        idx, sc = F.quantize_matrix(rng.standard_normal((k, n)).astype(np.float32), bits, 128)
+        hs.append(F.DeviceWeights(idx, sc, F.build_nf_table(bits), bits, 128))
+    items, want = [], []
+    for i, m in enumerate([1, 5, 32, 17, 3, 64]):
+        dw = hs[i % len(hs)]
+        x = (rng.standard_normal((m, dw.k)) * 0.5).astype(np.float16)
+        xd = torch.from_numpy(x).cuda()
+        want.append(dw.gemm(xd).cpu().numpy().view(np.uint16))
+        items.append((dw, x.view(np.uint16), np.zeros((m, dw.n), np.uint16)))
+    F.gemm_host_batch(items)
+    for (_, _, out), w in zip(items, want):
+        assert np.array_equal(out, w)
+    with pytest.raises(F.InputError):
+        F.gemm_host_batch([(hs[0], np.zeros((2, hs[0].k + 1), np.uint16), np.zeros((2, hs[0].n), np.uint16))])
+
+
+def test_mixed_m_on_one_handle_keeps_streamk_workspace_clean(F, gpu):
+    """Regression: the tcgen05 path's split-K partials share the handle's
+    workspace with the Stream-K fixup slots (zero = unwritten); a prefill-sized
+    call (M >= 64) between decode-sized calls must not perturb them."""
+    torch = gpu
+    rng = np.random.default_rng(5)
+    k, n = 384, 192
+    idx, sc = F.quantize_matrix(rng.standard_normal((k, n)).astype(np.float32), 2, 128)
+    dw = F.DeviceWeights(idx, sc, F.build_nf_table(2), 2, 128)
+    x32 = torch.from_numpy((rng.standard_normal((32, k)) * 0.5).astype(np.float16)).cuda()
+    x64 = torch.from_numpy((rng.standard_normal((64, k)) * 0.5).astype(np.float16)).cuda()
+    first = dw.gemm(x32).cpu().numpy().view(np.uint16)
+    big = dw.gemm(x64).cpu().numpy().view(np.uint16)
+    for _ in range(4):
+        assert np.array_equal(dw.gemm(x64).cpu().numpy().view(np.uint16), big)
+        assert np.array_equal(dw.gemm(x32).cpu().numpy().view(np.uint16), first)
