@@ -551,6 +551,39 @@ def execute(x16: np.ndarray, slices, k: int, n: int, bits: int, group: int, scal
     return MatmulResult(y, dict(zip(TRAFFIC_FIELDS, (int(v) for v in st))))
 
 
+class HostBatch:
+    """A prepared gemm_host_batch: validates the items and builds the C
+    argument arrays once; run() is then a single C call (input copies, GEMMs,
+    output copies).  The host arrays are referenced, not copied: refill them
+    in place between runs."""
+
+    def __init__(self, items, workers: int = 0):
+        cnt = len(items)
+        self._args = ((_vp * cnt)(), (C.c_void_p * cnt)(), (C.c_int * cnt)(),
+                      (C.c_void_p * cnt)())
+        hs, xs, ms, ys = self._args
+        self._keep = []
+        for i, (dw, x16, out) in enumerate(items):
+            if x16.dtype != np.uint16 or x16.ndim != 2 or x16.shape[1] != dw.k \
+                    or not x16.flags.c_contiguous:
+                raise InputError(f"item {i}: x must be a C-contiguous uint16 [m][{dw.k}] array")
+            if (out.dtype != np.uint16 or out.shape != (x16.shape[0], dw.n)
+                    or not out.flags.c_contiguous):
+                raise InputError(f"item {i}: out must be a C-contiguous uint16 [m][{dw.n}] array")
+            self._keep.append((dw, x16, out))
+            hs[i] = dw._h
+            xs[i] = x16.ctypes.data
+            ys[i] = out.ctypes.data
+            ms[i] = x16.shape[0]
+        self._cnt = cnt
+        self._workers = workers
+
+    def run(self, stream=None) -> None:
+        hs, xs, ms, ys = self._args
+        _check(_lib.flute_gemm_host_batch(hs, xs, ms, ys, self._cnt, self._workers,
+                                          _stream_ptr(stream)))
+
+
 def gemm_host_batch(items, workers: int = 0, stream=None) -> None:
     """End-to-end batch (flute_gemm_host_batch): items = [(DeviceWeights,
     x16 uint16 [m][k] host array, out uint16 [m][n] host array), ...].  Input
