@@ -357,30 +357,39 @@ def run_ours(args):
     batches = [F.HostBatch(e2e_items(s_)) for s_ in range(REPLICAS)]  # prepared once
     for b in batches:  # warm
         b.run(stream.cuda_stream)
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for s_ in range(e2e_steps):
-        batches[s_ % REPLICAS].run(stream.cuda_stream)
-    e2e_s = time.perf_counter() - t0
-    # the same through the one-GEMM-per-call host API (sync per GEMM)
-    t0 = time.perf_counter()
-    cnt = 0
-    for _ in range(e2e_steps):
-        for (m, k, n) in cases:
-            weights[(k, n)][cnt % REPLICAS].gemm_host(x_host[(m, k)], out=y_host[(m, n)])
-            cnt += 1
-    e2e_single_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * step_bytes * e2e_steps / e2e_s / 1e9
-    if world > 1:
-        t = torch.tensor([e2e_single_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_single_s = float(t.item())
-    e2e_single = world * step_bytes * e2e_steps / e2e_single_s / 1e9
+    def timed_rounds(fn, rounds=5):
+        """wall seconds per step of each round (max over ranks); the median is
+        reported, so one host hiccup does not decide the number"""
+        per = max(4, e2e_steps // rounds)
+        out = []
+        for r in range(rounds):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            fn(r * per, per)
+            dt = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t.item())
+            out.append(dt / per)
+        return out
+
+    def run_batches(s0, count):
+        for s_ in range(s0, s0 + count):
+            batches[s_ % REPLICAS].run(stream.cuda_stream)
+
+    def run_single(s0, count):
+        cnt = s0 * len(cases)
+        for _ in range(count):
+            for (m, k, n) in cases:
+                weights[(k, n)][cnt % REPLICAS].gemm_host(x_host[(m, k)], out=y_host[(m, n)])
+                cnt += 1
+
+    e2e_rounds = timed_rounds(run_batches)
+    single_rounds = timed_rounds(run_single)
+    e2e_value = world * step_bytes / statistics.median(e2e_rounds) / 1e9
+    e2e_single = world * step_bytes / statistics.median(single_rounds) / 1e9
     h2d = sum(m * k * 2 for (m, k, n) in cases)
     d2h = sum(m * n * 2 for (m, k, n) in cases)
 
@@ -419,6 +428,7 @@ def run_ours(args):
                             "in from pinned host memory and Y copied out, pipelined over copy "
                             "streams; wall clock, one synchronous call per step",
                     "steps": e2e_steps,
+                    "rounds_gbs": [round(world * step_bytes / t / 1e9, 1) for t in e2e_rounds],
                     "per_call_value": round(e2e_single, 2),
                     "per_call_path": "flute_gemm_host, one synchronous call per GEMM"},
             "gpu_launches": steps * len(cases),
