@@ -355,8 +355,9 @@ def run_ours(args):
                  y_host[(m, n)]) for i, (m, k, n) in enumerate(cases)]
 
     batches = [F.HostBatch(e2e_items(s_)) for s_ in range(REPLICAS)]  # prepared once
-    for b in batches:  # warm
-        b.run(stream.cuda_stream)
+    for _ in range(4):  # warm (first replays upload the graphs)
+        for b in batches:
+            b.run(stream.cuda_stream)
     def timed_rounds(fn, rounds=5):
         """wall seconds per step of each round (max over ranks); the median is
         reported, so one host hiccup does not decide the number"""

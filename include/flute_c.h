@@ -142,6 +142,17 @@ int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y
  * every output is in host memory.  Pinned host buffers make the copies DMA. */
 int flute_gemm_host_batch(flute_weights* const* ws, const uint16_t* const* x_host, const int* m,
                           uint16_t* const* y_host, int count, int workers, void* stream);
+/* The same batch prepared once and captured as a CUDA graph (copies in, GEMMs,
+ * copies out, with their cross-stream dependencies; own staging buffers).
+ * flute_host_batch_run replays it on `stream` and returns when every output
+ * is in host memory.  The handles and host buffers must outlive the batch;
+ * refill the inputs in place between runs. */
+typedef struct flute_host_batch flute_host_batch;
+int flute_host_batch_create(flute_weights* const* ws, const uint16_t* const* x_host, const int* m,
+                            uint16_t* const* y_host, int count, int workers,
+                            flute_host_batch** out);
+int flute_host_batch_run(flute_host_batch* b, void* stream);
+void flute_host_batch_destroy(flute_host_batch* b);
 
 /* ---- weight preparation on the device / FLTE ----------
  * flute_quantize_device: quantize_matrix (quantize.cpp:81-128) on the GPU for

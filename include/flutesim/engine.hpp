@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <vector>
 #include <string>
 
 #include "flutesim/matrix.hpp"
@@ -22,6 +23,11 @@
 #include "flutesim/quantize.hpp"
 #include "flutesim/streamk.hpp"
 #include "flutesim/vec_lut.hpp"
+
+namespace flute_dev {
+struct HostBatchItem;
+struct HostBatchGraph;
+}  // namespace flute_dev
 
 namespace flutesim {
 
@@ -165,12 +171,36 @@ class DeviceWeights {
   static void gemm_host_batch(DeviceWeights* const* ws, const std::uint16_t* const* x_host,
                               const int* m, std::uint16_t* const* y_host, int count,
                               int workers = 0, void* stream = nullptr);
+  // (internal) the per-item closures behind gemm_host_batch / HostBatch
+  static std::vector<flute_dev::HostBatchItem> batch_items(DeviceWeights* const* ws,
+                                                           const std::uint16_t* const* x_host,
+                                                           const int* m,
+                                                           std::uint16_t* const* y_host, int count,
+                                                           int workers);
 
   struct Impl;
 
  private:
   DeviceWeights();
   std::unique_ptr<Impl> impl_;
+};
+
+// A gemm_host_batch prepared once and captured as a CUDA graph: input copies
+// (from the given host buffers), the GEMMs and the output copies, with their
+// cross-stream dependencies.  run() replays it on `stream` and returns when
+// every output is on the host.  The handles and host buffers must outlive it;
+// refill the host inputs in place between runs.
+class HostBatch {
+ public:
+  HostBatch(DeviceWeights* const* ws, const std::uint16_t* const* x_host, const int* m,
+            std::uint16_t* const* y_host, int count, int workers = 0);
+  ~HostBatch();
+  HostBatch(const HostBatch&) = delete;
+  HostBatch& operator=(const HostBatch&) = delete;
+  void run(void* stream = nullptr);
+
+ private:
+  flute_dev::HostBatchGraph* graph_;
 };
 
 }  // namespace flutesim

@@ -132,6 +132,11 @@ _SIGS = {
                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "flute_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _vp]),
     "flute_gemm_host": (C.c_int, [_vp, _u16p, C.c_int, _u16p, C.c_int, _vp]),
+    "flute_host_batch_create": (C.c_int, [C.POINTER(_vp), C.POINTER(C.c_void_p),
+                                          C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.c_int,
+                                          C.c_int, C.POINTER(_vp)]),
+    "flute_host_batch_run": (C.c_int, [_vp, _vp]),
+    "flute_host_batch_destroy": (None, [_vp]),
     "flute_gemm_host_batch": (C.c_int, [C.POINTER(_vp), C.POINTER(C.c_void_p), C.POINTER(C.c_int),
                                         C.POINTER(C.c_void_p), C.c_int, C.c_int, _vp]),
     "flute_execute": (C.c_int, [_u16p, C.c_int, _u32p, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -552,12 +557,13 @@ def execute(x16: np.ndarray, slices, k: int, n: int, bits: int, group: int, scal
 
 
 class HostBatch:
-    """A prepared gemm_host_batch: validates the items and builds the C
-    argument arrays once; run() is then a single C call (input copies, GEMMs,
-    output copies).  The host arrays are referenced, not copied: refill them
-    in place between runs."""
+    """A prepared host-buffer batch (flute_host_batch_create): input copies,
+    GEMMs and output copies captured once as a CUDA graph; run() replays it
+    and returns when every output array is filled.  graph=False keeps the
+    eager pipelined path (flute_gemm_host_batch per run).  The host arrays
+    are referenced, not copied: refill the inputs in place between runs."""
 
-    def __init__(self, items, workers: int = 0):
+    def __init__(self, items, workers: int = 0, graph: bool = True):
         cnt = len(items)
         self._args = ((_vp * cnt)(), (C.c_void_p * cnt)(), (C.c_int * cnt)(),
                       (C.c_void_p * cnt)())
@@ -577,11 +583,25 @@ class HostBatch:
             ms[i] = x16.shape[0]
         self._cnt = cnt
         self._workers = workers
+        self._g = None
+        if graph:
+            g = _vp()
+            _check(_lib.flute_host_batch_create(hs, xs, ms, ys, cnt, workers, C.byref(g)))
+            self._g = g
 
     def run(self, stream=None) -> None:
+        if self._g is not None:
+            _check(_lib.flute_host_batch_run(self._g, _stream_ptr(stream)))
+            return
         hs, xs, ms, ys = self._args
         _check(_lib.flute_gemm_host_batch(hs, xs, ms, ys, self._cnt, self._workers,
                                           _stream_ptr(stream)))
+
+    def __del__(self):
+        g = getattr(self, "_g", None)
+        if g is not None and _lib is not None:
+            _lib.flute_host_batch_destroy(g)
+            self._g = None
 
 
 def gemm_host_batch(items, workers: int = 0, stream=None) -> None:

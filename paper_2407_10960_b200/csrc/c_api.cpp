@@ -616,6 +616,50 @@ int flute_gemm_host_batch(flute_weights* const* ws, const uint16_t* const* x_hos
   });
 }
 
+struct flute_host_batch {
+  HostBatch* impl = nullptr;
+};
+
+int flute_host_batch_create(flute_weights* const* ws, const uint16_t* const* x_host, const int* m,
+                            uint16_t* const* y_host, int count, int workers,
+                            flute_host_batch** out) {
+  return guard([&] {
+    need(out, "out");
+    if (count > 0) {
+      need(ws, "weights");
+      need(x_host, "x_host");
+      need(m, "m");
+      need(y_host, "y_host");
+    }
+    std::vector<DeviceWeights*> h(static_cast<std::size_t>(std::max(count, 0)));
+    for (int i = 0; i < count; ++i) {
+      need(ws[i], "weights[i]");
+      h[i] = ws[i]->impl;
+    }
+    auto* b = new flute_host_batch();
+    try {
+      b->impl = new HostBatch(h.data(), x_host, m, y_host, count, workers);
+    } catch (...) {
+      delete b;
+      throw;
+    }
+    *out = b;
+  });
+}
+
+int flute_host_batch_run(flute_host_batch* b, void* stream) {
+  return guard([&] {
+    need(b, "batch");
+    b->impl->run(stream);
+  });
+}
+
+void flute_host_batch_destroy(flute_host_batch* b) {
+  if (!b) return;
+  delete b->impl;
+  delete b;
+}
+
 int flute_gemm_host(flute_weights* w, const uint16_t* x_host, int m, uint16_t* y_host,
                     int workers, void* stream) {
   return guard([&] {

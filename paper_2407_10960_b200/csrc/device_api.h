@@ -118,12 +118,19 @@ class SteDevice {
 // output is in host memory.  gemm(x_dev, y_dev, stream) enqueues one GEMM.
 struct HostBatchItem {
   std::function<void(const void*, void*, void*)> gemm;
+  std::function<void()> prepare;  // size the handle's workspace (before capture)
   const void* x_host = nullptr;
   std::size_t x_bytes = 0;
   void* y_host = nullptr;
   std::size_t y_bytes = 0;
 };
 void host_batch(const std::vector<HostBatchItem>& items, void* stream);
+// The same batch captured once into a CUDA graph (own staging buffers and
+// copy streams); run replays it on `stream` and synchronises.
+struct HostBatchGraph;
+HostBatchGraph* host_batch_capture(const std::vector<HostBatchItem>& items);
+void host_batch_run(HostBatchGraph* g, void* stream);
+void host_batch_free(HostBatchGraph* g);
 
 // Small RAII device buffer helpers used by the host layer.
 void* dev_alloc(std::size_t bytes);

@@ -162,15 +162,21 @@ struct DeviceWeights::Impl {
 
   static int mclass(int m) { return m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : -1; }
 
-  void gemm(const void* x, int m, void* y, int workers, void* stream,
-            void* const* y_peers = nullptr, int n_peers = 0, int ldy = 0, int ycol0 = 0,
-            const flute_dev::Decomp* force = nullptr) {
+  // grow the workspace for an (m, workers) call (a synchronous allocation:
+  // never inside CUDA-graph capture)
+  void ensure_ws(int m, int workers) {
     const std::size_t need = flute_dev::call_workspace_bytes(m, k, n, workers);
     if (need > ws.bytes) {
       ws = DeviceBuffer(need);
       flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
       flute_dev::stream_sync(nullptr);
     }
+  }
+
+  void gemm(const void* x, int m, void* y, int workers, void* stream,
+            void* const* y_peers = nullptr, int n_peers = 0, int ldy = 0, int ycol0 = 0,
+            const flute_dev::Decomp* force = nullptr) {
+    ensure_ws(m, workers);
     flute_dev::GemmArgs a;
     a.x = x;
     a.m = m;
@@ -365,9 +371,9 @@ void DeviceWeights::gemm_host_raw(const std::uint16_t* x_host, int m, std::uint1
   flute_dev::stream_sync(stream);
 }
 
-void DeviceWeights::gemm_host_batch(DeviceWeights* const* ws, const std::uint16_t* const* x_host,
-                                    const int* m, std::uint16_t* const* y_host, int count,
-                                    int workers, void* stream) {
+std::vector<flute_dev::HostBatchItem> DeviceWeights::batch_items(
+    DeviceWeights* const* ws, const std::uint16_t* const* x_host, const int* m,
+    std::uint16_t* const* y_host, int count, int workers) {
   if (count < 0) throw ConfigError("gemm_host_batch: count must be >= 0");
   std::vector<flute_dev::HostBatchItem> items(static_cast<std::size_t>(count));
   for (int i = 0; i < count; ++i) {
@@ -379,13 +385,29 @@ void DeviceWeights::gemm_host_batch(DeviceWeights* const* ws, const std::uint16_
     items[i].gemm = [im, mi, workers](const void* x, void* y, void* st) {
       im->gemm(x, mi, y, workers, st);
     };
+    items[i].prepare = [im, mi, workers]() { im->ensure_ws(mi, workers); };
     items[i].x_host = x_host[i];
     items[i].x_bytes = static_cast<std::size_t>(mi) * im->k * 2;
     items[i].y_host = y_host[i];
     items[i].y_bytes = static_cast<std::size_t>(mi) * im->n * 2;
   }
-  flute_dev::host_batch(items, stream);
+  return items;
 }
+
+void DeviceWeights::gemm_host_batch(DeviceWeights* const* ws, const std::uint16_t* const* x_host,
+                                    const int* m, std::uint16_t* const* y_host, int count,
+                                    int workers, void* stream) {
+  flute_dev::host_batch(batch_items(ws, x_host, m, y_host, count, workers), stream);
+}
+
+HostBatch::HostBatch(DeviceWeights* const* ws, const std::uint16_t* const* x_host, const int* m,
+                     std::uint16_t* const* y_host, int count, int workers)
+    : graph_(flute_dev::host_batch_capture(
+          DeviceWeights::batch_items(ws, x_host, m, y_host, count, workers))) {}
+
+HostBatch::~HostBatch() { flute_dev::host_batch_free(graph_); }
+
+void HostBatch::run(void* stream) { flute_dev::host_batch_run(graph_, stream); }
 
 // ---------------------------------------------------------------------------
 // Reference API

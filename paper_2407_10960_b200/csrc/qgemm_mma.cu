@@ -684,6 +684,122 @@ struct BatchCtx {
 };
 }  // namespace
 
+namespace {
+// Enqueue the batch: copies in on h2d, GEMMs on st, copies out on d2h.  In
+// capture mode there is no event query (illegal while capturing): inputs are
+// waited for in doubling groups; in eager mode an input already resident is
+// not waited for at all.
+void enqueue_batch(const std::vector<HostBatchItem>& items, uint8_t* base,
+                   const std::vector<size_t>& xo, const std::vector<size_t>& yo, cudaStream_t st,
+                   cudaStream_t h2d, cudaStream_t d2h, cudaEvent_t start,
+                   const std::vector<cudaEvent_t>& in_ready,
+                   const std::vector<cudaEvent_t>& out_ready, bool capturing) {
+  FLUTE_CUDA(cudaEventRecord(start, st));
+  FLUTE_CUDA(cudaStreamWaitEvent(h2d, start, 0));
+  for (size_t i = 0; i < items.size(); ++i) {
+    FLUTE_CUDA(cudaMemcpyAsync(base + xo[i], items[i].x_host, items[i].x_bytes,
+                               cudaMemcpyHostToDevice, h2d));
+    FLUTE_CUDA(cudaEventRecord(in_ready[i], h2d));
+  }
+  // Each wait node between two GEMMs costs their programmatic-launch overlap,
+  // so GEMM 0 waits for input 0 and GEMM i (i = 1, 2, 4, ...) for inputs up to
+  // 2i + 1 — copies run far ahead of the GEMMs (an M <= 32 input is <= 1 MB).
+  static const bool wait_each = std::getenv("FLUTE_BATCH_WAIT_EACH") != nullptr;
+  long covered = -1;
+  for (size_t i = 0; i < items.size(); ++i) {
+    if (static_cast<long>(i) > covered) {
+      const size_t j = wait_each || i == 0 ? i : std::min(items.size() - 1, 2 * i + 1);
+      if (capturing || cudaEventQuery(in_ready[j]) != cudaSuccess)
+        FLUTE_CUDA(cudaStreamWaitEvent(st, in_ready[j], 0));
+      covered = static_cast<long>(j);
+    }
+    items[i].gemm(base + xo[i], base + yo[i], st);
+    FLUTE_CUDA(cudaEventRecord(out_ready[i], st));
+    FLUTE_CUDA(cudaStreamWaitEvent(d2h, out_ready[i], 0));
+    FLUTE_CUDA(cudaMemcpyAsync(items[i].y_host, base + yo[i], items[i].y_bytes,
+                               cudaMemcpyDeviceToHost, d2h));
+  }
+}
+
+size_t batch_layout(const std::vector<HostBatchItem>& items, std::vector<size_t>& xo,
+                    std::vector<size_t>& yo) {
+  xo.resize(items.size());
+  yo.resize(items.size());
+  size_t total = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    xo[i] = total;
+    total += (items[i].x_bytes + 255) / 256 * 256;
+    yo[i] = total;
+    total += (items[i].y_bytes + 255) / 256 * 256;
+  }
+  return total;
+}
+}  // namespace
+
+struct HostBatchGraph {
+  void* arena = nullptr;
+  cudaStream_t cap = nullptr, h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> events;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+void host_batch_free(HostBatchGraph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  for (cudaEvent_t e : g->events) cudaEventDestroy(e);
+  if (g->cap) cudaStreamDestroy(g->cap);
+  if (g->h2d) cudaStreamDestroy(g->h2d);
+  if (g->d2h) cudaStreamDestroy(g->d2h);
+  if (g->arena) cudaFree(g->arena);
+  delete g;
+}
+
+HostBatchGraph* host_batch_capture(const std::vector<HostBatchItem>& items) {
+  auto* g = new HostBatchGraph();
+  try {
+    for (const auto& it : items)
+      if (it.prepare) it.prepare();  // workspace growth is not capturable
+    std::vector<size_t> xo, yo;
+    const size_t total = batch_layout(items, xo, yo);
+    FLUTE_CUDA(cudaMalloc(&g->arena, total ? total : 256));
+    FLUTE_CUDA(cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking));
+    FLUTE_CUDA(cudaStreamCreateWithFlags(&g->h2d, cudaStreamNonBlocking));
+    FLUTE_CUDA(cudaStreamCreateWithFlags(&g->d2h, cudaStreamNonBlocking));
+    const size_t n = items.size();
+    g->events.resize(2 * n + 2);
+    for (auto& e : g->events) FLUTE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    std::vector<cudaEvent_t> in(g->events.begin(), g->events.begin() + n);
+    std::vector<cudaEvent_t> out(g->events.begin() + n, g->events.begin() + 2 * n);
+    FLUTE_CUDA(cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_batch(items, static_cast<uint8_t*>(g->arena), xo, yo, g->cap, g->h2d, g->d2h,
+                    g->events[2 * n], in, out, true);
+      // join the copy-out stream back into the origin stream
+      FLUTE_CUDA(cudaEventRecord(g->events[2 * n + 1], g->d2h));
+      FLUTE_CUDA(cudaStreamWaitEvent(g->cap, g->events[2 * n + 1], 0));
+    } catch (...) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(g->cap, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    FLUTE_CUDA(cudaStreamEndCapture(g->cap, &g->graph));
+    FLUTE_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+  } catch (...) {
+    host_batch_free(g);
+    throw;
+  }
+  return g;
+}
+
+void host_batch_run(HostBatchGraph* g, void* stream) {
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FLUTE_CUDA(cudaGraphLaunch(g->exec, st));
+  FLUTE_CUDA(cudaStreamSynchronize(st));
+}
+
 void host_batch(const std::vector<HostBatchItem>& items, void* stream) {
   if (items.empty()) return;
   static thread_local std::vector<BatchCtx> ctxs;
@@ -692,46 +808,15 @@ void host_batch(const std::vector<HostBatchItem>& items, void* stream) {
   if (static_cast<int>(ctxs.size()) <= dev) ctxs.resize(dev + 1);
   BatchCtx& c = ctxs[dev];
   if (c.dev < 0) c.init(dev);
-  c.events(items.size());
+  c.events(items.size() + 1);
+  for (const auto& it : items)
+    if (it.prepare) it.prepare();
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  std::vector<size_t> xo(items.size()), yo(items.size());
-  size_t total = 0;
-  for (size_t i = 0; i < items.size(); ++i) {
-    xo[i] = total;
-    total += (items[i].x_bytes + 255) / 256 * 256;
-    yo[i] = total;
-    total += (items[i].y_bytes + 255) / 256 * 256;
-  }
-  uint8_t* base = static_cast<uint8_t*>(c.staging(total));
-  // copies in: ordered after whatever the caller queued on its stream
-  cudaEvent_t start = c.out_ready[0];
-  FLUTE_CUDA(cudaEventRecord(start, st));
-  FLUTE_CUDA(cudaStreamWaitEvent(c.h2d, start, 0));
-  for (size_t i = 0; i < items.size(); ++i) {
-    FLUTE_CUDA(cudaMemcpyAsync(base + xo[i], items[i].x_host, items[i].x_bytes,
-                               cudaMemcpyHostToDevice, c.h2d));
-    FLUTE_CUDA(cudaEventRecord(c.in_ready[i], c.h2d));
-  }
-  // Each wait node between two GEMMs costs their programmatic-launch overlap,
-  // so inputs are waited for in doubling groups: GEMM 0 waits for input 0,
-  // GEMM i (i = 1, 2, 4, ...) for inputs up to 2i + 1 — copies run far ahead of
-  // the GEMMs (an M <= 32 input is <= 1 MB), so the later waits are free.
-  static const bool wait_each = std::getenv("FLUTE_BATCH_WAIT_EACH") != nullptr;
-  long covered = -1;
+  std::vector<size_t> xo, yo;
+  uint8_t* base = static_cast<uint8_t*>(c.staging(batch_layout(items, xo, yo)));
   try {
-    for (size_t i = 0; i < items.size(); ++i) {
-      if (static_cast<long>(i) > covered) {
-        const size_t j = wait_each || i == 0 ? i : std::min(items.size() - 1, 2 * i + 1);
-        if (cudaEventQuery(c.in_ready[j]) != cudaSuccess)
-          FLUTE_CUDA(cudaStreamWaitEvent(st, c.in_ready[j], 0));
-        covered = static_cast<long>(j);
-      }
-      items[i].gemm(base + xo[i], base + yo[i], stream);
-      FLUTE_CUDA(cudaEventRecord(c.out_ready[i], st));
-      FLUTE_CUDA(cudaStreamWaitEvent(c.d2h, c.out_ready[i], 0));
-      FLUTE_CUDA(cudaMemcpyAsync(items[i].y_host, base + yo[i], items[i].y_bytes,
-                                 cudaMemcpyDeviceToHost, c.d2h));
-    }
+    enqueue_batch(items, base, xo, yo, st, c.h2d, c.d2h, c.in_ready[items.size()], c.in_ready,
+                  c.out_ready, false);
   } catch (...) {
     // drain what was queued before the failure so the arena is free again
     cudaStreamSynchronize(c.h2d);

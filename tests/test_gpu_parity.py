@@ -399,3 +399,29 @@ def test_mixed_m_on_one_handle_keeps_streamk_workspace_clean(F, gpu):
     for _ in range(4):
         assert np.array_equal(dw.gemm(x64).cpu().numpy().view(np.uint16), big)
         assert np.array_equal(dw.gemm(x32).cpu().numpy().view(np.uint16), first)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_host_batch_object_replays(F, gpu, graph):
+    """HostBatch (CUDA-graph capture of copies + GEMMs + copies, or the eager
+    pipelined path) gives the device path's bits, including an M >= 64
+    (tcgen05) item, and picks up refilled inputs on every run."""
+    torch = gpu
+    rng = np.random.default_rng(7)
+    hs = []
+    for (k, n, bits) in [(256, 320, 3), (512, 256, 4)]:
+        idx, sc = F.quantize_matrix(rng.standard_normal((k, n)).astype(np.float32), bits, 128)
+        hs.append(F.DeviceWeights(idx, sc, F.build_nf_table(bits), bits, 128))
+    ms = [1, 16, 64, 32]
+    xs = [np.zeros((m, hs[i % 2].k), np.uint16) for i, m in enumerate(ms)]
+    outs = [np.zeros((m, hs[i % 2].n), np.uint16) for i, m in enumerate(ms)]
+    batch = F.HostBatch([(hs[i % 2], xs[i], outs[i]) for i in range(len(ms))], graph=graph)
+    for rep in range(3):
+        want = []
+        for i, m in enumerate(ms):
+            x = (rng.standard_normal((m, hs[i % 2].k)) * 0.5).astype(np.float16)
+            xs[i][...] = x.view(np.uint16)
+            want.append(hs[i % 2].gemm(torch.from_numpy(x).cuda()).cpu().numpy().view(np.uint16))
+        batch.run()
+        for o, w in zip(outs, want):
+            assert np.array_equal(o, w), rep
