@@ -16,3 +16,7 @@ NCU_PROFILING=1 timeout 600 ncu --set full --clock-control none --import-source 
   -o $O/prof_w3_m1_4096x14336 python tools/profile_case.py 1 4096 14336 3 128 8 > $O/ncu_w3.log 2>&1; tail -2 $O/ncu_w3.log
 NCU_PROFILING=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:qgemm -s 4 -c 2 \
   -o $O/prof_w4_m1_4096x4096 python tools/profile_case.py 1 4096 4096 4 128 8 > $O/ncu_w4.log 2>&1; tail -2 $O/ncu_w4.log
+NCU_PROFILING=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:qgemm -s 4 -c 1 \
+  -o $O/prof_w3_m32_4096x14336 python tools/profile_case.py 32 4096 14336 3 128 8 > $O/ncu_w3m32.log 2>&1; tail -2 $O/ncu_w3m32.log
+timeout 300 python tools/perf_tc.py > $O/perf_tc.txt 2>&1; cat $O/perf_tc.txt
+timeout 300 python tools/perf_refine.py 4096 4096 128 > $O/perf_refine.txt 2>&1; cat $O/perf_refine.txt
