@@ -26,6 +26,11 @@ struct GemmArgs {
   int ldy = 0, ycol0 = 0;
   void* workspace = nullptr;
   std::size_t workspace_bytes = 0;
+  // Optional separate buffer for the tcgen05 path's split-K partials (M >= 64).
+  // Without it the partials go to `workspace`, which the Stream-K path also
+  // uses, and the reduce kernel must re-zero them (slower).
+  void* tc_part = nullptr;
+  std::size_t tc_part_bytes = 0;
   int workers = 0;               // <= 0: default
   void* stream = nullptr;
   // Decomposition override (autotuner): cluster >= 1 forces cluster split-K
@@ -51,7 +56,9 @@ void qgemm(const GemmArgs& a);
 // workspace; tc_workspace_bytes is the size for the full split count.
 bool tc_enabled(int m);
 std::size_t tc_workspace_bytes(int m, int k, int n, int sms);
-void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, void* part,
+// Split-K partial bytes of the tcgen05 path for an m-row call (0 if m < 64).
+std::size_t tc_call_part_bytes(int m, int k, int n);
+void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool zero_part, void* part,
               std::size_t part_bytes);
 // Workspace a qgemm call with these dimensions needs (either path).
 std::size_t call_workspace_bytes(int m, int k, int n, int workers);

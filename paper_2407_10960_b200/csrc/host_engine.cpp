@@ -129,7 +129,7 @@ struct DeviceBuffer {
 
 struct DeviceWeights::Impl {
   int k = 0, n = 0, bits = 0, group = 0;
-  DeviceBuffer w, sc, lut, ws, xbuf, ybuf;
+  DeviceBuffer w, sc, lut, ws, ws_tc, xbuf, ybuf;
 
   void upload(const std::vector<std::uint8_t>& packed, const std::vector<std::uint16_t>& scales,
               const std::vector<std::uint32_t>& lut_words) {
@@ -155,6 +155,15 @@ struct DeviceWeights::Impl {
       flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
       flute_dev::stream_sync(nullptr);
     }
+    for (int m = 64; m <= max_m; m = m < 512 ? m * 2 : m + 512) grow_tc(m);
+    grow_tc(max_m);
+  }
+
+  // the tcgen05 path's split-K partials: a buffer of their own, so the
+  // Stream-K slots in `ws` are never touched by M >= 64 calls
+  void grow_tc(int m) {
+    const std::size_t need = flute_dev::tc_call_part_bytes(m, k, n);
+    if (need > ws_tc.bytes) ws_tc = DeviceBuffer(need);
   }
 
   // autotuned decomposition per m-class (row block 8 / 16 / 32), -1 = none
@@ -171,6 +180,7 @@ struct DeviceWeights::Impl {
       flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
       flute_dev::stream_sync(nullptr);
     }
+    grow_tc(m);
   }
 
   void gemm(const void* x, int m, void* y, int workers, void* stream,
@@ -190,6 +200,8 @@ struct DeviceWeights::Impl {
     a.y = y;
     a.workspace = ws.p;
     a.workspace_bytes = ws.bytes;
+    a.tc_part = ws_tc.p;
+    a.tc_part_bytes = ws_tc.bytes;
     a.workers = workers;
     a.stream = stream;
     a.y_peers = y_peers;

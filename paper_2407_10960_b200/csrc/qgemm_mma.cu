@@ -404,6 +404,10 @@ std::vector<Decomp> decomp_candidates(int m, int k, int n) {
   return out;
 }
 
+size_t tc_call_part_bytes(int m, int k, int n) {
+  return tc_enabled(m) ? tc_workspace_bytes(m, k, n, props().sms) : 0;
+}
+
 size_t call_workspace_bytes(int m, int k, int n, int workers) {
   const size_t mma = workspace_bytes(std::min(m, 32), workers > 0 ? workers : max_workers(std::min(m, 32)) * 4);
   return tc_enabled(m) ? std::max(mma, tc_workspace_bytes(m, k, n, props().sms)) : mma;
@@ -446,7 +450,10 @@ void qgemm(const GemmArgs& a) {
   const int gp = kp / a.group;
   if (a.n_peers == 0 && tc_enabled(a.m)) {
     // compute-bound regime: one tcgen05 launch over all rows
-    qgemm_tc(a, tiles_k, np / kUnitN, gp, props().sms, a.workspace, a.workspace_bytes);
+    if (a.tc_part)
+      qgemm_tc(a, tiles_k, np / kUnitN, gp, props().sms, false, a.tc_part, a.tc_part_bytes);
+    else
+      qgemm_tc(a, tiles_k, np / kUnitN, gp, props().sms, true, a.workspace, a.workspace_bytes);
     return;
   }
   // M > 32: 32-row chunks, stream-ordered on one workspace.

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "dequant.cuh"
 #include "device_api.h"
@@ -109,15 +110,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BITS, int BN>
+// KD = stage depth: 128 (one unit per stage, two 64-k swizzle atoms) or 64
+// (half a unit: one atom, so a BN = 256 X tile still double-buffers within
+// shared memory; the 8 dequant warps then split as 2 units x 4 k-steps).
+template <int BITS, int BN, int KD>
 __global__ void __launch_bounds__(kThreads, 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int kSubBytes = BITS * 1024;
-  constexpr uint32_t kABytes = 2 * 16384;   // two 64-k swizzle atoms of 128 rows
+  static_assert(KD == 128 || KD == 64, "stage depth");
+  constexpr int kAtoms = KD / 64;             // 64-k swizzle atoms per stage
+  constexpr int kSubBytes = BITS * 1024;      // one unit's packed weights
+  constexpr int kStageW = kSubBytes * KD / 128;  // per unit per stage
+  constexpr uint32_t kABytes = kAtoms * 16384;   // kAtoms 64-k swizzle atoms of 128 rows
   constexpr uint32_t kXBox = BN * 128;      // one 64-k box of BN rows
-  constexpr uint32_t kWOff = kABytes + 2 * kXBox;
-  constexpr uint32_t kSOff = kWOff + 2 * kSubBytes;
+  constexpr uint32_t kWOff = kABytes + kAtoms * kXBox;
+  constexpr uint32_t kSOff = kWOff + 2 * kStageW;
 
   const uint32_t base = smem_u32(smem);
   const uint32_t lut = base;
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int z = blockIdx.z;
   const int kt_lo = z * p.tiles_k / p.splits;
   const int kt_hi = (z + 1) * p.tiles_k / p.splits;
-  const int nk = kt_hi - kt_lo;
+  const int nk = (kt_hi - kt_lo) * (128 / KD);  // stages
   const int nt0 = 2 * pair;
   const bool has_u1 = nt0 + 1 < p.tiles_n;
 
@@ -171,22 +178,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol = policy_evict_first();
       const int units_pair = has_u1 ? 2 : 1;
       for (int i = 0, s = 0, ph = 0; i < nk; ++i) {
-        const int kt = kt_lo + i;
+        const int kt = kt_lo + i / (128 / KD);
+        const int half = KD == 64 ? (i & 1) : 0;  // which 64-k half of the unit
         if (i >= S) mbar_wait(empty(s), ph ^ 1);
         const uint32_t st = stage(s);
         const int glo = (kt * kUnitK) >> p.group_shift;
         const uint32_t sb = p.ng * 128;
-        mbar_arrive_expect_tx(full_w(s), units_pair * (kSubBytes + sb));
+        mbar_arrive_expect_tx(full_w(s), units_pair * (kStageW + sb));
         for (int u = 0; u < units_pair; ++u) {
           const size_t unit = static_cast<size_t>(nt0 + u) * p.tiles_k + kt;
-          bulk_g2s_hint(st + kWOff + u * kSubBytes, p.w + unit * kSubBytes, kSubBytes, full_w(s), pol);
+          const uint8_t* wu = p.w + unit * kSubBytes;
+          if constexpr (KD == 128) {
+            bulk_g2s_hint(st + kWOff + u * kStageW, wu, kSubBytes, full_w(s), pol);
+          } else if constexpr (BITS == 3) {
+            // k-steps 4h..4h+3: 2-bit plane bytes [1024h, +1024), 1-bit [2048 + 512h, +512)
+            bulk_g2s_hint(st + kWOff + u * kStageW, wu + 1024 * half, 1024, full_w(s), pol);
+            bulk_g2s_hint(st + kWOff + u * kStageW + 1024, wu + 2048 + 512 * half, 512, full_w(s), pol);
+          } else {
+            bulk_g2s_hint(st + kWOff + u * kStageW, wu + kStageW * half, kStageW, full_w(s), pol);
+          }
           bulk_g2s(st + kSOff + u * sb, p.sc + (static_cast<size_t>(nt0 + u) * p.gp + glo) * 128, sb,
                    full_w(s));
         }
         if (i == 0) pdl_wait();  // X belongs to the previous kernel in the stream
-        mbar_arrive_expect_tx(full_x(s), 2 * kXBox);
-        tma_2d_g2s(st + kABytes, &tmap_x, kt * kUnitK, m0, full_x(s));
-        tma_2d_g2s(st + kABytes + kXBox, &tmap_x, kt * kUnitK + 64, m0, full_x(s));
+        mbar_arrive_expect_tx(full_x(s), kAtoms * kXBox);
+#pragma unroll
+        for (int a = 0; a < kAtoms; ++a)
+          tma_2d_g2s(st + kABytes + a * kXBox, &tmap_x, kt * kUnitK + 64 * (half + a), m0, full_x(s));
         if (++s == S) {
           s = 0;
           ph ^= 1;
@@ -203,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t st = stage(s);
       if (elect_one()) {
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int a = 0; a < kAtoms; ++a)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = smem_desc_sw128(st + a * 16384 + kk * 32);
@@ -224,34 +242,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     fill_lut<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
     named_bar_sync(1, kDqWarps * 32);
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
-    const int kstep = warp;
-    const int slot = kstep * 32 + lane;
+    // KD = 128: warp w owns k-step w of both units; KD = 64: k-step (w & 3) of
+    // the stage's half of unit w >> 2 (local k-step kl within the stage)
+    constexpr int kUnitsPerWarp = KD == 128 ? 2 : 1;
+    const int kl = KD == 128 ? warp : (warp & 3);
+    const int u0 = KD == 128 ? 0 : (warp >> 2);
+    const int slot = kl * 32 + lane;  // this lane's slot within the stage's weight bytes
     const int g = lane >> 2, t = lane & 3;
     // A-tile byte offset of this lane's pair p of atom j, unit u (row n, k = kk, kk+1)
     auto a_off = [&](int u, int j, int pp) -> uint32_t {
       const int n = 64 * u + 16 * j + g + 8 * (pp & 1);
-      const int kk = 16 * kstep + 2 * t + 8 * (pp >> 1);
+      const int kk = 16 * kl + 2 * t + 8 * (pp >> 1);
       const int at = kk >> 6, kin = kk & 63;
       return static_cast<uint32_t>(at * 16384 + (n >> 3) * 1024 + (n & 7) * 128 +
                                    ((((kin >> 3) ^ (n & 7))) << 4) + (kin & 7) * 2);
     };
-    uint32_t aoff[2][4][4];
+    uint32_t aoff[kUnitsPerWarp][4][4];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int uu = 0; uu < kUnitsPerWarp; ++uu)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) aoff[u][j][pp] = a_off(u, j, pp);
+        for (int pp = 0; pp < 4; ++pp) aoff[uu][j][pp] = a_off(u0 + uu, j, pp);
     const uint32_t s_lane = (lane >> 2) * 16;
     for (int i = 0, s = 0, ph = 0; i < nk; ++i) {
-      const int kt = kt_lo + i;
+      const int kt = kt_lo + i / (128 / KD);
+      const int kstep = KD == 128 ? kl : kl + 4 * (i & 1);  // k-step within the unit
       mbar_wait(full_w(s), ph);
       const uint32_t st = stage(s);
       const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt << 7) >> p.group_shift);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int uu = 0; uu < kUnitsPerWarp; ++uu) {
+        const int u = u0 + uu;
         if (u == 1 && !has_u1) break;
-        const uint32_t wr = st + kWOff + u * kSubBytes;
+        const uint32_t wr = st + kWOff + u * kStageW;
         LaneBits<BITS> lb;
         if constexpr (BITS == 4) {
           lb.w = lds128(wr + slot * 16);
@@ -259,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           lb.w = lds64(wr + slot * 8);
         } else {
           lb.hi = lds64(wr + slot * 8);
-          lb.lo = lds32(wr + 2048 + slot * 4);
+          lb.lo = lds32(wr + kStageW * 2 / 3 + slot * 4);  // 1-bit plane after the 2-bit plane
         }
         const uint4 sq = lds128(st + kSOff + u * p.ng * 128 + gl * 128 + s_lane);
 #pragma unroll
@@ -268,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t a[4];
           lut_dequant4(atom_index_bytes<BITS>(lb, j), lane4, lut, scw, a);
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) sts32(st + aoff[u][j][pp], a[pp]);
+          for (int pp = 0; pp < 4; ++pp) sts32(st + aoff[uu][j][pp], a[pp]);
         }
       }
       fence_proxy_async_smem();  // generic-proxy A stores -> visible to the tensor core
@@ -319,18 +343,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Sums the split partials in fixed split order and re-zeroes them: the
 // workspace is shared with the Stream-K path, whose slots must read zero
 // ("unwritten") at rest (qgemm_kernel.cuh fixup protocol).
+// (only when the partials live in that shared workspace: ZERO).
+template <bool ZERO>
 __global__ void splitk_reduce_kernel(float* __restrict__ part, __half* __restrict__ y, int splits,
                                      size_t mn) {
   pdl_wait();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < mn;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float acc = part[i];
-    part[i] = 0.f;
-    for (int z = 1; z < splits; ++z) {
-      acc += part[static_cast<size_t>(z) * mn + i];
-      part[static_cast<size_t>(z) * mn + i] = 0.f;
-    }
+    for (int z = 1; z < splits; ++z) acc += part[static_cast<size_t>(z) * mn + i];
     y[i] = __float2half_rn(acc);
+    if (ZERO)
+      for (int z = 0; z < splits; ++z) part[static_cast<size_t>(z) * mn + i] = 0.f;
   }
 }
 
@@ -366,16 +390,17 @@ EncodeTiledTc encode_tc() {
 
 struct TcPlan {
   int bn = 128, splits = 1, stages = 2;
+  bool zero_part = false;
   size_t smem = 0;
   tc::Params prm{};
 };
 
-template <int BITS, int BN>
+template <int BITS, int BN, int KD>
 void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
   static thread_local int configured = -1;
   int dev = 0;
   FLUTE_TC_CUDA(cudaGetDevice(&dev));
-  auto kern = tc::qgemm_tc_kernel<BITS, BN>;
+  auto kern = tc::qgemm_tc_kernel<BITS, BN, KD>;
   if (configured != dev) {
     int optin = 0;
     FLUTE_TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -413,28 +438,48 @@ void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
     c2.stream = stream;
     c2.attrs = attr;
     c2.numAttrs = 1;
-    FLUTE_TC_CUDA(cudaLaunchKernelEx(&c2, tc::splitk_reduce_kernel, pl.prm.part,
-                                     static_cast<__half*>(a.y), pl.splits, mn));
+    if (pl.zero_part)
+      FLUTE_TC_CUDA(cudaLaunchKernelEx(&c2, tc::splitk_reduce_kernel<true>, pl.prm.part,
+                                       static_cast<__half*>(a.y), pl.splits, mn));
+    else
+      FLUTE_TC_CUDA(cudaLaunchKernelEx(&c2, tc::splitk_reduce_kernel<false>, pl.prm.part,
+                                       static_cast<__half*>(a.y), pl.splits, mn));
   }
 }
 
 }  // namespace
 
+// X rows per CTA: 64 / 128, or 256 (UMMA N = 256 with 64-deep stages) when
+// 128-row tiles would need more than one wave of CTAs — each dequantised W^T
+// tile then feeds twice as many rows (measured: 8192^2 M=512 123 -> 79 us;
+// with a single wave of 128-row tiles BN = 128 stays faster, e.g. 4096^2
+// M=512 34 vs 38 us, because BN = 256 would then need split-K).
+int tc_bn(int m, int tiles_n, int sms) {
+  if (std::getenv("FLUTE_TC_BN")) return std::atoi(std::getenv("FLUTE_TC_BN"));
+  if (m < 128) return 64;
+  const long tiles128 = static_cast<long>((tiles_n + 1) / 2) * ((m + 127) / 128);
+  return m >= 256 && tiles128 > sms ? 256 : 128;
+}
+
 size_t tc_workspace_bytes(int m, int k, int n, int sms) {
   const int tiles_n = (n + 63) / 64;
   const int tiles_k = (k + 127) / 128;
-  const int bn = m >= 128 ? 128 : 64;
+  const int bn = tc_bn(m, tiles_n, sms);
   const long tiles = static_cast<long>((tiles_n + 1) / 2) * ((m + bn - 1) / bn);
-  const int splits = static_cast<int>(std::max<long>(1, std::min<long>(std::min(tiles_k, 8), sms / std::max<long>(tiles, 1))));
+  int splits = static_cast<int>(std::max<long>(1, std::min<long>(std::min(tiles_k, 8), sms / std::max<long>(tiles, 1))));
+  if (const char* f = std::getenv("FLUTE_TC_SPLITS")) splits = std::max(1, std::min(tiles_k, std::atoi(f)));
   return splits > 1 ? static_cast<size_t>(splits) * m * n * 4 : 0;
 }
 
 bool tc_enabled(int m) { return m >= 64 && std::getenv("FLUTE_NO_TC") == nullptr; }
 
-void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, void* part,
-              size_t part_bytes) {
+void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool zero_part,
+              void* part, size_t part_bytes) {
   TcPlan pl;
-  pl.bn = a.m >= 128 ? 128 : 64;
+  pl.zero_part = zero_part;
+  pl.bn = tc_bn(a.m, tiles_n, sms);
+  if (pl.bn != 64 && pl.bn != 128 && pl.bn != 256) throw flutesim::ConfigError("FLUTE_TC_BN must be 64, 128 or 256");
+  const int kd = pl.bn == 256 ? 64 : 128;
   const long tiles = static_cast<long>((tiles_n + 1) / 2) * ((a.m + pl.bn - 1) / pl.bn);
   pl.splits = static_cast<int>(
       std::max<long>(1, std::min<long>(std::min(tiles_k, 8), sms / std::max<long>(tiles, 1))));
@@ -444,9 +489,10 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, void
   const size_t lut = static_cast<size_t>(1u << (2 * a.bits)) * kLutRowBytes;
   const size_t bar_off = lut;
   const size_t stage_off = (bar_off + 8 * (4 * tc::kMaxStages + 2) + 1023) / 1024 * 1024;
-  const size_t stage_bytes =
-      ((2 * 16384 + 2 * static_cast<size_t>(pl.bn) * 128 + 2 * a.bits * 1024 + 2 * ng * 128) + 1023) /
-      1024 * 1024;
+  const size_t atoms = kd / 64;
+  const size_t stage_bytes = ((atoms * 16384 + atoms * static_cast<size_t>(pl.bn) * 128 +
+                               2 * static_cast<size_t>(a.bits) * 1024 * kd / 128 + 2 * ng * 128) +
+                              1023) / 1024 * 1024;
   int optin = 0, dev = 0;
   FLUTE_TC_CUDA(cudaGetDevice(&dev));
   FLUTE_TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -473,11 +519,16 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, void
   p.stage_off = static_cast<uint32_t>(stage_off);
   p.stage_bytes = static_cast<uint32_t>(stage_bytes);
   cudaStream_t st = static_cast<cudaStream_t>(a.stream);
-  const bool bn128 = pl.bn == 128;
+  auto go = [&](auto bits_tag) {
+    constexpr int B = decltype(bits_tag)::value;
+    if (pl.bn == 256) launch_tc<B, 256, 64>(a, pl, st);
+    else if (pl.bn == 128) launch_tc<B, 128, 128>(a, pl, st);
+    else launch_tc<B, 64, 128>(a, pl, st);
+  };
   switch (a.bits) {
-    case 2: bn128 ? launch_tc<2, 128>(a, pl, st) : launch_tc<2, 64>(a, pl, st); break;
-    case 3: bn128 ? launch_tc<3, 128>(a, pl, st) : launch_tc<3, 64>(a, pl, st); break;
-    default: bn128 ? launch_tc<4, 128>(a, pl, st) : launch_tc<4, 64>(a, pl, st); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    default: go(std::integral_constant<int, 4>{}); break;
   }
 }
 

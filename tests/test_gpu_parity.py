@@ -268,6 +268,24 @@ TC_CASES = [  # (m, k, n, bits, group, splits) — compute-bound tcgen05 path (m
     (128, 512, 384, 2, 256, 1), (200, 384, 320, 4, 128, 3), (256, 1024, 128, 3, 128, 0),
     (512, 2048, 512, 4, 128, 0), (65, 128, 64, 2, 32, 1),
 ]
+# UMMA N = 256 with 64-deep stages (chosen when 128-row tiles need more than one
+# wave; forced here): W2/W3/W4, a partial second row block, an odd 64-column
+# tile count, group 32 and split K
+TC256_CASES = [(300, 512, 192, 3, 32, 0), (256, 384, 320, 2, 64, 3), (512, 1024, 256, 4, 256, 2),
+               (257, 256, 64, 4, 128, 1), (512, 2048, 1024, 4, 128, 0)]
+
+
+@pytest.mark.parametrize("m,k,n,bits,group,splits", TC256_CASES)
+def test_qgemm_tcgen05_n256_vs_oracle(F, orc, gpu, monkeypatch, m, k, n, bits, group, splits):
+    monkeypatch.setenv("FLUTE_TC_BN", "256")
+    if splits:
+        monkeypatch.setenv("FLUTE_TC_SPLITS", str(splits))
+    rng = np.random.default_rng(7000 + m + k + n + bits + group)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, emax, ratio = _within(y16, y64)
+    assert ok, f"max err {emax:.4g} ({ratio:.2f} of bound)"
 
 
 @pytest.mark.parametrize("m,k,n,bits,group,splits", TC_CASES)
