@@ -71,6 +71,8 @@ SMALL = [  # (m, k, n, bits, group)
     (1, 512, 256, 3, 128), (7, 256, 128, 3, 32), (32, 384, 320, 3, 64),
     (1, 256, 128, 2, 128), (12, 512, 64, 2, 256), (3, 128, 64, 2, 32),
     (1, 64, 16, 4, 32), (2, 48 * 8, 80, 4, 128), (33, 256, 128, 4, 128), (70, 256, 192, 3, 128),
+    # W3 with 9..16 rows: two units per stage (BM = 16)
+    (16, 512, 192, 3, 32), (10, 1152, 320, 3, 128), (13, 384, 64, 3, 64),
 ]
 
 
@@ -98,6 +100,21 @@ def test_qgemm_workers_sweep_vs_reference_engine(F, orc, gpu, workers):
     yref, _ = orc.execute(x16, slices, k, n, bits, group, scales, table, workers=min(workers, 8))
     ok, err, _ = _within(y16, yref.view(np.float16).astype(np.float64))
     assert ok, err
+
+
+@pytest.mark.parametrize("workers", [1, 5, 37, 148, 300])
+def test_qgemm_w3_m16_workers_sweep(F, orc, gpu, workers):
+    """W3 with 9..16 rows (two units per stage): odd Stream-K ranges split a
+    stage's unit pair; same bound, bitwise reproducible."""
+    rng = np.random.default_rng(300 + workers)
+    m, k, n, bits, group = 14, 1664, 320, 3, 128   # 13 k-units: odd per tile
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group, workers=workers)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, err, ratio = _within(y16, y64)
+    assert ok, f"max err {err:.4g} ({ratio:.2f}x bound)"
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    assert np.array_equal(dw.gemm(x, workers=workers).cpu().numpy().view(np.uint16), y16)
 
 
 def test_qgemm_deterministic_and_split_free_bitwise(F, orc, gpu):
@@ -222,6 +239,7 @@ def test_gpu_error_paths(F, orc, gpu):
 BASE = [  # BASELINE.json configs at full size (parity by the same bound)
     (1, 4096, 4096, 4, 128), (16, 4096, 4096, 4, 128),
     (1, 4096, 14336, 3, 128), (32, 4096, 14336, 3, 128), (4, 14336, 4096, 3, 128),
+    (16, 4096, 14336, 3, 128), (16, 14336, 4096, 3, 128),
     (1, 8192, 8192, 2, 256), (8, 8192, 8192, 4, 32),
     (1, 8192, 28672, 4, 128),                        # configs[3] layer (1 GPU)
     (128, 4096, 4096, 4, 128), (512, 2048, 4096, 4, 128),  # configs[4] (tcgen05 path)
@@ -246,7 +264,8 @@ def test_qgemm_baseline_shapes(F, orc, gpu, m, k, n, bits, group):
 
 @pytest.mark.parametrize("m,k,n,bits,group,cluster", [
     (1, 512, 256, 4, 128, 2), (5, 1024, 128, 3, 64, 4), (16, 1024, 192, 4, 32, 8),
-    (32, 768, 128, 2, 256, 2), (3, 256, 64, 3, 128, 2), (9, 2048, 64, 4, 128, 1)])
+    (32, 768, 128, 2, 256, 2), (3, 256, 64, 3, 128, 2), (9, 2048, 64, 4, 128, 1),
+    (12, 1024, 128, 3, 64, 4), (16, 2048, 64, 3, 32, 8)])
 def test_qgemm_cluster_splitk(F, orc, gpu, monkeypatch, m, k, n, bits, group, cluster):
     """Cluster split-K mode (one cluster per 64-column tile, DSMEM reduction),
     forced on small shapes; same bound as the Stream-K path, and bitwise
