@@ -287,18 +287,33 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 template <int BITS>
 void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp, int cluster) {
+  // W3 (the 3-bit planes make a unit's stage copy small): larger stages when the
+  // shared-memory plan still keeps >= 3 of them — M <= 8 four units per stage
+  // (measured up to 5 % faster than two), M = 9..16 two (3-4 % faster than
+  // one).  W2 / W4 (the latter's 64 KB vLUT leaves too few stages) keep the
+  // smaller stages; M = 32 keeps two units (one measured 7-10 % slower).
   switch (bm_for(m_rows)) {
-    case 8: launch_impl<BITS, 8, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
-    case 16:
-      // W3: two units per stage when that still leaves >= 3 stages (measured
-      // 3-4 % faster than one unit; W2 measured 1 % slower, W4's 64 KB vLUT
-      // leaves too few stages)
-      if (BITS == 3 && plan_smem<BITS, 16, 2, 8>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3)
-        launch_impl<BITS, 16, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
-      else
-        launch_impl<BITS, 16, 1, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+    case 8:
+      if constexpr (BITS == 3) {
+        if (plan_smem<BITS, 8, 4, 8>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
+          launch_impl<BITS, 8, 4, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+          break;
+        }
+      }
+      launch_impl<BITS, 8, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
       break;
-    default: launch_impl<BITS, 32, 2, 1, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+    case 16:
+      if constexpr (BITS == 3) {
+        if (plan_smem<BITS, 16, 2, 8>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
+          launch_impl<BITS, 16, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+          break;
+        }
+      }
+      launch_impl<BITS, 16, 1, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+      break;
+    default:
+      launch_impl<BITS, 32, 2, 1, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+      break;
   }
 }
 

@@ -71,8 +71,9 @@ SMALL = [  # (m, k, n, bits, group)
     (1, 512, 256, 3, 128), (7, 256, 128, 3, 32), (32, 384, 320, 3, 64),
     (1, 256, 128, 2, 128), (12, 512, 64, 2, 256), (3, 128, 64, 2, 32),
     (1, 64, 16, 4, 32), (2, 48 * 8, 80, 4, 128), (33, 256, 128, 4, 128), (70, 256, 192, 3, 128),
-    # W3 with 9..16 rows: two units per stage (BM = 16)
+    # W3 with 9..16 rows: two units per stage (BM = 16); <= 8 rows: four
     (16, 512, 192, 3, 32), (10, 1152, 320, 3, 128), (13, 384, 64, 3, 64),
+    (1, 1152, 192, 3, 32), (8, 896, 320, 3, 128), (3, 640, 64, 3, 64),
 ]
 
 
@@ -102,12 +103,13 @@ def test_qgemm_workers_sweep_vs_reference_engine(F, orc, gpu, workers):
     assert ok, err
 
 
+@pytest.mark.parametrize("m", [14, 5])
 @pytest.mark.parametrize("workers", [1, 5, 37, 148, 300])
-def test_qgemm_w3_m16_workers_sweep(F, orc, gpu, workers):
-    """W3 with 9..16 rows (two units per stage): odd Stream-K ranges split a
-    stage's unit pair; same bound, bitwise reproducible."""
-    rng = np.random.default_rng(300 + workers)
-    m, k, n, bits, group = 14, 1664, 320, 3, 128   # 13 k-units: odd per tile
+def test_qgemm_w3_workers_sweep(F, orc, gpu, workers, m):
+    """W3 with multi-unit stages (M <= 8: four units, 9..16: two): odd
+    Stream-K ranges split a stage; same bound, bitwise reproducible."""
+    rng = np.random.default_rng(300 + workers + m)
+    k, n, bits, group = 1664, 320, 3, 128   # 13 k-units: odd per tile
     idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
     y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group, workers=workers)
     y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
@@ -265,7 +267,8 @@ def test_qgemm_baseline_shapes(F, orc, gpu, m, k, n, bits, group):
 @pytest.mark.parametrize("m,k,n,bits,group,cluster", [
     (1, 512, 256, 4, 128, 2), (5, 1024, 128, 3, 64, 4), (16, 1024, 192, 4, 32, 8),
     (32, 768, 128, 2, 256, 2), (3, 256, 64, 3, 128, 2), (9, 2048, 64, 4, 128, 1),
-    (12, 1024, 128, 3, 64, 4), (16, 2048, 64, 3, 32, 8)])
+    (12, 1024, 128, 3, 64, 4), (16, 2048, 64, 3, 32, 8), (2, 1536, 128, 3, 128, 4),
+    (7, 2048, 64, 3, 32, 8)])
 def test_qgemm_cluster_splitk(F, orc, gpu, monkeypatch, m, k, n, bits, group, cluster):
     """Cluster split-K mode (one cluster per 64-column tile, DSMEM reduction),
     forced on small shapes; same bound as the Stream-K path, and bitwise
