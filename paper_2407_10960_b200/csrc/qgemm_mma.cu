@@ -724,33 +724,69 @@ void enqueue_batch(const std::vector<HostBatchItem>& items, uint8_t* base,
                    cudaStream_t h2d, cudaStream_t d2h, cudaEvent_t start,
                    const std::vector<cudaEvent_t>& in_ready,
                    const std::vector<cudaEvent_t>& out_ready, bool capturing) {
+  // Every cross-stream dependency on the GEMM stream costs two consecutive
+  // GEMMs their programmatic-launch overlap, and every copy ~4 us of fixed
+  // cost, so copies are grouped: inputs in groups growing from the front
+  // ([0,2), [2,4), [4,8), ...: the first GEMM starts early, later inputs are
+  // far ahead of the GEMMs — an M <= 32 input is <= 1 MB), outputs in groups
+  // shrinking towards the back (..., [n-4,n-2), [n-2,n-1), [n-1,n): little is
+  // left to copy after the last GEMM).  A group's copies are merged where its
+  // items' host buffers are adjacent (a step's inputs / outputs allocated back
+  // to back, as bench.py does); the staging layout keeps the device side
+  // adjacent.  FLUTE_BATCH_WAIT_EACH=1: one item per group.
+  static const bool each = std::getenv("FLUTE_BATCH_WAIT_EACH") != nullptr;
+  const size_t n = items.size();
+  std::vector<char> in_start(n + 1, 0), out_end(n + 1, 0);
+  for (size_t b = 0; b < n; b = each ? b + 1 : std::max<size_t>(2, 2 * b)) in_start[b] = 1;
+  out_end[n] = 1;  // output groups end at n, n-1, n-2, n-4, ... (sizes 1, 1, 2, 4, ...)
+  for (size_t k = 1; k < n; k = each ? k + 1 : 2 * k) out_end[n - k] = 1;
+  auto copy_range = [&](size_t a, size_t b, bool in) {
+    for (size_t i = a; i < b;) {
+      const uint8_t* h = static_cast<const uint8_t*>(in ? items[i].x_host : items[i].y_host);
+      uint8_t* d = base + (in ? xo[i] : yo[i]);
+      size_t bytes = in ? items[i].x_bytes : items[i].y_bytes;
+      size_t j = i + 1;
+      for (; j < b; ++j) {
+        const uint8_t* hj = static_cast<const uint8_t*>(in ? items[j].x_host : items[j].y_host);
+        if (hj != h + bytes || base + (in ? xo[j] : yo[j]) != d + bytes) break;
+        bytes += in ? items[j].x_bytes : items[j].y_bytes;
+      }
+      if (in)
+        FLUTE_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, h2d));
+      else
+        FLUTE_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(h), d, bytes, cudaMemcpyDeviceToHost, d2h));
+      i = j;
+    }
+  };
   FLUTE_CUDA(cudaEventRecord(start, st));
   FLUTE_CUDA(cudaStreamWaitEvent(h2d, start, 0));
-  for (size_t i = 0; i < items.size(); ++i) {
-    FLUTE_CUDA(cudaMemcpyAsync(base + xo[i], items[i].x_host, items[i].x_bytes,
-                               cudaMemcpyHostToDevice, h2d));
-    FLUTE_CUDA(cudaEventRecord(in_ready[i], h2d));
+  std::vector<size_t> in_ev(n, 0);  // input group event of each group start
+  size_t ev = 0;
+  for (size_t a = 0; a < n;) {
+    size_t b = a + 1;
+    while (b < n && !in_start[b]) ++b;
+    copy_range(a, b, true);
+    FLUTE_CUDA(cudaEventRecord(in_ready[ev], h2d));
+    in_ev[a] = ev++;
+    a = b;
   }
-  // Each wait node between two GEMMs costs their programmatic-launch overlap,
-  // so GEMM 0 waits for input 0 and GEMM i (i = 1, 2, 4, ...) for inputs up to
-  // 2i + 1 — copies run far ahead of the GEMMs (an M <= 32 input is <= 1 MB).
-  static const bool wait_each = std::getenv("FLUTE_BATCH_WAIT_EACH") != nullptr;
-  long covered = -1;
-  for (size_t i = 0; i < items.size(); ++i) {
-    if (static_cast<long>(i) > covered) {
-      const size_t j = wait_each || i == 0 ? i : std::min(items.size() - 1, 2 * i + 1);
-      if (capturing || cudaEventQuery(in_ready[j]) != cudaSuccess)
-        FLUTE_CUDA(cudaStreamWaitEvent(st, in_ready[j], 0));
-      covered = static_cast<long>(j);
-    }
+  size_t oev = 0, out_a = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (in_start[i] && (capturing || cudaEventQuery(in_ready[in_ev[i]]) != cudaSuccess))
+      FLUTE_CUDA(cudaStreamWaitEvent(st, in_ready[in_ev[i]], 0));
     items[i].gemm(base + xo[i], base + yo[i], st);
-    FLUTE_CUDA(cudaEventRecord(out_ready[i], st));
-    FLUTE_CUDA(cudaStreamWaitEvent(d2h, out_ready[i], 0));
-    FLUTE_CUDA(cudaMemcpyAsync(items[i].y_host, base + yo[i], items[i].y_bytes,
-                               cudaMemcpyDeviceToHost, d2h));
+    if (out_end[i + 1]) {
+      FLUTE_CUDA(cudaEventRecord(out_ready[oev], st));
+      FLUTE_CUDA(cudaStreamWaitEvent(d2h, out_ready[oev], 0));
+      ++oev;
+      copy_range(out_a, i + 1, false);
+      out_a = i + 1;
+    }
   }
 }
 
+// Staging: all inputs back to back, then all outputs (each 256-byte aligned),
+// so items adjacent in host memory are adjacent on the device too.
 size_t batch_layout(const std::vector<HostBatchItem>& items, std::vector<size_t>& xo,
                     std::vector<size_t>& yo) {
   xo.resize(items.size());
@@ -759,6 +795,8 @@ size_t batch_layout(const std::vector<HostBatchItem>& items, std::vector<size_t>
   for (size_t i = 0; i < items.size(); ++i) {
     xo[i] = total;
     total += (items[i].x_bytes + 255) / 256 * 256;
+  }
+  for (size_t i = 0; i < items.size(); ++i) {
     yo[i] = total;
     total += (items[i].y_bytes + 255) / 256 * 256;
   }
