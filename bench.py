@@ -343,13 +343,18 @@ def run_ours(args):
 
     # ---- end-to-end through the C ABI with (pinned) host buffers ----
     e2e_steps = max(3, min(200, args.steps // 20))
-    # a step's inputs back to back in one pinned buffer, outputs in another
-    # (in case order), so the host batch can move each group of them with one copy
+    # The step's 8 GEMMs are independent, so the host batch runs them in the
+    # order that best overlaps the copies with the GEMMs — Johnson's rule for
+    # the copy-in -> copy-out flow shop: items whose input is no larger than
+    # their output first (ascending input), then the rest (descending output).
+    # Their inputs sit back to back in one pinned buffer and their outputs in
+    # another, in that order, so each copy group is a single transfer.
+    e2e_order = sorted(cases, key=lambda c: (0, c[0] * c[1]) if c[1] <= c[2] else (1, -c[0] * c[2]))
     x_arena = torch.empty(sum(m * k for (m, k, _) in cases), dtype=torch.float16).pin_memory()
     y_arena = torch.empty(sum(m * n for (m, _, n) in cases), dtype=torch.float16).pin_memory()
     x_host, y_host = {}, {}
     xo = yo = 0
-    for (m, k, n) in cases:
+    for (m, k, n) in e2e_order:
         x_host[(m, k)] = x_arena[xo:xo + m * k].numpy().view(np.uint16).reshape(m, k)
         x_host[(m, k)][...] = xs[(m, k)].cpu().numpy().view(np.uint16)
         y_host[(m, n)] = y_arena[yo:yo + m * n].numpy().view(np.uint16).reshape(m, n)
@@ -360,7 +365,7 @@ def run_ours(args):
     # pipelined with the GEMMs; the call returns with all outputs on the host
     def e2e_items(step):
         return [(weights[(k, n)][(step * len(cases) + i) % REPLICAS], x_host[(m, k)],
-                 y_host[(m, n)]) for i, (m, k, n) in enumerate(cases)]
+                 y_host[(m, n)]) for i, (m, k, n) in enumerate(e2e_order)]
 
     batches = [F.HostBatch(e2e_items(s_)) for s_ in range(REPLICAS)]  # prepared once
     for _ in range(4):  # warm (first replays upload the graphs)
