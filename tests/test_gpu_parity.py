@@ -465,3 +465,31 @@ def test_host_batch_object_replays(F, gpu, graph):
         batch.run()
         for o, w in zip(outs, want):
             assert np.array_equal(o, w), rep
+
+
+def _random_w3_cases(count=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        m = int(rng.integers(1, 17))
+        k = 128 * int(rng.integers(1, 24))
+        n = 64 * int(rng.integers(1, 12)) - (16 if rng.random() < 0.3 else 0)
+        group = int(rng.choice([32, 64, 128, 256]))
+        while k % group:
+            group //= 2
+        workers = int(rng.choice([0, 0, 1, 3, 29, 148, 296]))
+        out.append((m, k, n, group, workers))
+    return out
+
+
+@pytest.mark.parametrize("m,k,n,group,workers", _random_w3_cases())
+def test_qgemm_w3_random_shapes(F, orc, gpu, m, k, n, group, workers):
+    """Randomised W3 shapes through the multi-unit-stage kernels (M <= 16):
+    ragged k-unit counts, partial 64-column tiles, every group size, default
+    and explicit Stream-K worker counts."""
+    rng = np.random.default_rng(m * 1000003 + k * 101 + n + group + workers)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, 3, group)
+    y16, _ = _gemm(F, gpu, idx, scales, table, x16, 3, group, workers=workers)
+    y64 = orc.reference_f64(x16, idx, 3, group, scales, table)
+    ok, err, ratio = _within(y16, y64)
+    assert ok, f"max err {err:.4g} ({ratio:.2f}x bound)"
