@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 template <int CHAINS>
 __global__ void hmma_f32(int iters, float* out) {
@@ -122,6 +123,62 @@ __global__ void lut_mma_loop(int iters, float* out) {
   float s = 0.f;
   for (int j = 0; j < 4; ++j) for (int r = 0; r < 4; ++r) s += acc[j][r];
   if (s == 1.2345f || sink == 0x1234567u) out[0] = s;
+}
+
+// The same loop for MT 8-row m-tiles of X per atom (M = 8*MT rows): each atom's
+// dequantised A feeds MT HMMAs with different B fragments (the M = 16 / 32
+// kernels), 4*MT accumulators per atom column.
+template <int MT>
+__global__ void lut_mma_loop_mt(int iters, float* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint32_t* w = reinterpret_cast<uint32_t*>(sm);
+  for (int i = threadIdx.x; i < 65536 / 4 + 8192; i += blockDim.x) w[i] = i * 2654435761u;
+  __syncthreads();
+  const uint32_t lut = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+  const uint32_t data = lut + 65536;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lane4 = lane * 4;
+  float acc[MT][4][4] = {};
+  for (int i = 0; i < iters; ++i) {
+    const uint32_t off = data + ((i * 8 + warp) & 63) * 512;
+    uint4 lb, sq;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(lb.x), "=r"(lb.y), "=r"(lb.z), "=r"(lb.w) : "r"(off + lane * 16));
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(sq.x), "=r"(sq.y), "=r"(sq.z), "=r"(sq.w) : "r"(off + (lane >> 2) * 16));
+    uint32_t b[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];" : "=r"(b[mt][0]), "=r"(b[mt][1]) : "r"(off + ((lane + 16 * mt) & 31) * 16));
+    uint32_t v[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t idx = j == 0 ? lb.x : j == 1 ? lb.y : j == 2 ? lb.z : lb.w;
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        uint32_t o;
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(o) : "r"(idx), "r"(lane4), "r"(0x5504u | (pp << 4)));
+        asm("ld.shared.u32 %0, [%1];" : "=r"(v[j][pp]) : "r"(lut + o));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t scw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
+      const __half2 s2 = *reinterpret_cast<const __half2*>(&scw);
+      uint32_t a[4];
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v[j][pp]), (pp & 1) ? __high2half2(s2) : __low2half2(s2));
+        a[pp] = *reinterpret_cast<const uint32_t*>(&r);
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+        asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(acc[mt][j][0]), "+f"(acc[mt][j][1]), "+f"(acc[mt][j][2]), "+f"(acc[mt][j][3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[mt][0]), "r"(b[mt][1]));
+    }
+  }
+  float s = 0.f;
+  for (int mt = 0; mt < MT; ++mt) for (int j = 0; j < 4; ++j) for (int r = 0; r < 4; ++r) s += acc[mt][j][r];
+  if (s == 1.2345f) out[0] = s;
 }
 
 // mbarrier costs: (a) try_wait on an already-completed phase, (b) a
@@ -318,6 +375,14 @@ int main() {
     cudaDeviceSynchronize();
   }
   const size_t sm = 65536 + 32768 + 1024;
+  if (getenv("MT_ONLY")) {
+    for (int th : {256, 384, 512}) {
+      run("MT=1 (M<=8)", lut_mma_loop_mt<1>, th, sm, 4.0, "T atoms/s", it / 4);
+      run("MT=2 (M=16)", lut_mma_loop_mt<2>, th, sm, 4.0, "T atoms/s", it / 4);
+      run("MT=4 (M=32)", lut_mma_loop_mt<4>, th, sm, 4.0, "T atoms/s", it / 4);
+    }
+    return 0;
+  }
   for (int th : {256, 512}) {
     run("full, 4 atoms/iter", lut_mma_loop<0, 4>, th, sm, 4.0, "T atoms/s", it / 4);
     run("full, 8 atoms/iter", lut_mma_loop<0, 8>, th, sm, 8.0, "T atoms/s", it / 8);
