@@ -95,7 +95,8 @@ double flute_bits_per_param(int bits, int group);
 int flute_device_count(void);
 int flute_sm_count(int device);
 /* Largest Stream-K CTA count that is guaranteed co-resident for an m-row call
- * (the finisher/contributor handshake needs every CTA resident). */
+ * at any bit width (W2/W3 with 17..32 rows allow twice this); larger counts
+ * are legal (ticketed worker ids keep the handshake deadlock-free). */
 int flute_max_workers(int m);
 /* Default worker count (CTAs) for a shape. */
 int flute_default_workers(int m, int k, int n, int bits);

@@ -322,7 +322,7 @@ int flute_sm_count(int device) {
 
 int flute_max_workers(int m) {
   int v = -1;
-  if (guard([&] { v = flute_dev::max_workers(m); }) != FLUTE_OK) return -1;
+  if (guard([&] { v = flute_dev::max_workers(m, 4); }) != FLUTE_OK) return -1;
   return v;
 }
 

@@ -43,7 +43,7 @@ struct GemmArgs {
 struct Decomp {
   int cluster = -1, workers = 0;
 };
-std::vector<Decomp> decomp_candidates(int m, int k, int n);
+std::vector<Decomp> decomp_candidates(int m, int k, int n, int bits);
 // Mean device time (us) of `fn` (one launch sequence on `stream`), each rep
 // preceded by an untimed write of a buffer larger than L2 so weights stream
 // from HBM as in real use.
@@ -63,7 +63,8 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
 // Workspace a qgemm call with these dimensions needs (either path).
 std::size_t call_workspace_bytes(int m, int k, int n, int workers);
 std::size_t workspace_bytes(int m, int workers);
-int max_workers(int m);
+// co-resident CTA slots of the memory-bound kernel for an m-row call
+int max_workers(int m, int bits = 3);
 int default_workers(int m, int k, int n, int bits);
 int sm_count(int device);
 int device_count();

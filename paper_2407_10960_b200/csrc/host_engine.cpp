@@ -322,7 +322,7 @@ std::string DeviceWeights::autotune(int m, void* stream, int reps) {
   if (reps < 1) reps = 1;
   DeviceBuffer x(static_cast<std::size_t>(m) * im.k * 2), y(static_cast<std::size_t>(m) * im.n * 2);
   flute_dev::dev_zero(x.p, x.bytes, stream);
-  const std::vector<flute_dev::Decomp> cands = flute_dev::decomp_candidates(m, im.k, im.n);
+  const std::vector<flute_dev::Decomp> cands = flute_dev::decomp_candidates(m, im.k, im.n, im.bits);
   for (const flute_dev::Decomp& c : cands) {  // grow the workspace before timing
     if (c.cluster == 0) {
       const std::size_t need = flute_dev::workspace_bytes(m, c.workers);

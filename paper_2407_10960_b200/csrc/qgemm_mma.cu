@@ -312,6 +312,22 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
       launch_impl<BITS, 16, 1, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
       break;
     default:
+      // M = 17..32: W2/W3 run two CTAs per SM with four consumer warps each
+      // (the register budget of two 8-warp CTAs does not fit): a launch's CTAs
+      // then hand their SM slots to the next launch one by one (PDL) instead of
+      // all at once — measured 7-11 % faster than one 8-warp CTA per SM.  W4's
+      // 64 KB vLUT leaves no room for two CTAs' pipelines.
+      if constexpr (BITS != 4) {
+        if (plan_smem<BITS, 32, 2, 4>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
+          launch_impl<BITS, 32, 2, 2, 4>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+          break;
+        }
+        if (plan_smem<BITS, 32, 1, 4>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
+          launch_impl<BITS, 32, 1, 2, 4>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+          break;
+        }
+        // (big cluster receive buffers: the one-CTA-per-SM kernel below)
+      }
       launch_impl<BITS, 32, 2, 1, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
       break;
   }
@@ -321,9 +337,9 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 // DSMEM reduction) when the tile count T fills >= 3/4 of the SMs with
 // T*C <= #SMs; returns C (1 = no split), or 0 for Stream-K.
 // CTAs per SM the kernel for an m-row launch is built for (launch_bits).
-int occ_for(int m) { return bm_for(std::min(m, 32)) <= 16 ? 2 : 1; }
+int occ_for(int m, int bits) { return bm_for(std::min(m, 32)) <= 16 || bits != 4 ? 2 : 1; }
 
-int cluster_for(long long tiles_n, int tiles_k, int m) {
+int cluster_for(long long tiles_n, int tiles_k, int m, int bits) {
   if (std::getenv("FLUTE_NO_CLUSTER")) return 0;
   if (const char* f = std::getenv("FLUTE_FORCE_CLUSTER")) {  // tests: force cluster size C
     const int c = std::atoi(f);
@@ -331,7 +347,7 @@ int cluster_for(long long tiles_n, int tiles_k, int m) {
   }
   // capacity: all co-resident CTA slots (two per SM for the OCC = 2 kernels,
   // measured faster than leaving the second slot to the next launch)
-  const int sms = props().sms * occ_for(m);
+  const int sms = props().sms * occ_for(m, bits);
   for (int c = 8; c >= 1; c /= 2) {
     if (c > tiles_k) continue;
     const long long g = tiles_n * c;
@@ -354,8 +370,8 @@ int sm_count(int device) {
   return v;
 }
 
-int max_workers(int m) {
-  return props().sms * occ_for(m);  // co-resident CTA slots
+int max_workers(int m, int bits) {
+  return props().sms * occ_for(m, bits);  // co-resident CTA slots
 }
 
 int default_workers(int m, int k, int n, int bits) {
@@ -363,9 +379,9 @@ int default_workers(int m, int k, int n, int bits) {
   (void)bits;
   const int tiles_k = (k + kUnitK - 1) / kUnitK;
   const long long tiles_n = (n + kUnitN - 1) / kUnitN;
-  const int c = cluster_for(tiles_n, tiles_k, m);
+  const int c = cluster_for(tiles_n, tiles_k, m, bits);
   if (c > 0) return static_cast<int>(tiles_n * c);
-  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, max_workers(m)));
+  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, max_workers(m, bits)));
 }
 
 void debug_times(unsigned long long* out, int workers) {
@@ -414,11 +430,11 @@ double time_launches(const std::function<void()>& fn, int reps, void* stream) {
   return total_ms * 1e3 / reps;
 }
 
-std::vector<Decomp> decomp_candidates(int m, int k, int n) {
+std::vector<Decomp> decomp_candidates(int m, int k, int n, int bits) {
   std::vector<Decomp> out;
   const int tiles_k = (k + kUnitK - 1) / kUnitK;
   const long long tiles_n = (n + kUnitN - 1) / kUnitN;
-  const int slots = max_workers(std::min(m, 32));
+  const int slots = max_workers(std::min(m, 32), bits);
   out.push_back({-1, 0});  // the heuristic's own choice
   for (int c = 1; c <= 8; c *= 2)
     if (c <= tiles_k && tiles_n * c <= slots && 2 * tiles_n * c >= slots) out.push_back({c, 0});
@@ -432,7 +448,8 @@ size_t tc_call_part_bytes(int m, int k, int n) {
 }
 
 size_t call_workspace_bytes(int m, int k, int n, int workers) {
-  const size_t mma = workspace_bytes(std::min(m, 32), workers > 0 ? workers : max_workers(std::min(m, 32)) * 4);
+  // (sized for the larger co-residency of any bit width)
+  const size_t mma = workspace_bytes(std::min(m, 32), workers > 0 ? workers : max_workers(std::min(m, 32), 3) * 4);
   return tc_enabled(m) ? std::max(mma, tc_workspace_bytes(m, k, n, props().sms)) : mma;
 }
 
@@ -461,7 +478,7 @@ void qgemm(const GemmArgs& a) {
   int cluster = a.cluster >= 1   ? std::min(a.cluster, tiles_k)
                 : a.cluster == 0 ? 0
                 : a.workers > 0  ? 0
-                                 : cluster_for(np / kUnitN, tiles_k, a.m);
+                                 : cluster_for(np / kUnitN, tiles_k, a.m, a.bits);
   if (a.cluster == 0 && a.workers <= 0) cluster = 0;
   int workers = cluster > 0 ? static_cast<int>(np / kUnitN) * cluster
                             : (a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits));

@@ -268,7 +268,8 @@ def test_qgemm_baseline_shapes(F, orc, gpu, m, k, n, bits, group):
     (1, 512, 256, 4, 128, 2), (5, 1024, 128, 3, 64, 4), (16, 1024, 192, 4, 32, 8),
     (32, 768, 128, 2, 256, 2), (3, 256, 64, 3, 128, 2), (9, 2048, 64, 4, 128, 1),
     (12, 1024, 128, 3, 64, 4), (16, 2048, 64, 3, 32, 8), (2, 1536, 128, 3, 128, 4),
-    (7, 2048, 64, 3, 32, 8)])
+    (7, 2048, 64, 3, 32, 8), (32, 2048, 192, 3, 32, 8), (24, 1024, 128, 2, 64, 4),
+    (20, 1024, 64, 4, 128, 2)])
 def test_qgemm_cluster_splitk(F, orc, gpu, monkeypatch, m, k, n, bits, group, cluster):
     """Cluster split-K mode (one cluster per 64-column tile, DSMEM reduction),
     forced on small shapes; same bound as the Stream-K path, and bitwise
@@ -467,11 +468,11 @@ def test_host_batch_object_replays(F, gpu, graph):
             assert np.array_equal(o, w), rep
 
 
-def _random_w3_cases(count=24, seed=2024):
+def _random_w3_cases(count=32, seed=2024):
     rng = np.random.default_rng(seed)
     out = []
     for _ in range(count):
-        m = int(rng.integers(1, 17))
+        m = int(rng.integers(1, 33))
         k = 128 * int(rng.integers(1, 24))
         n = 64 * int(rng.integers(1, 12)) - (16 if rng.random() < 0.3 else 0)
         group = int(rng.choice([32, 64, 128, 256]))
@@ -484,9 +485,10 @@ def _random_w3_cases(count=24, seed=2024):
 
 @pytest.mark.parametrize("m,k,n,group,workers", _random_w3_cases())
 def test_qgemm_w3_random_shapes(F, orc, gpu, m, k, n, group, workers):
-    """Randomised W3 shapes through the multi-unit-stage kernels (M <= 16):
-    ragged k-unit counts, partial 64-column tiles, every group size, default
-    and explicit Stream-K worker counts."""
+    """Randomised W3 shapes through the M <= 32 kernels (multi-unit stages for
+    M <= 16, two 4-warp CTAs per SM for 17..32): ragged k-unit counts, partial
+    64-column tiles, every group size, default and explicit Stream-K worker
+    counts."""
     rng = np.random.default_rng(m * 1000003 + k * 101 + n + group + workers)
     idx, scales, table, x16 = _case(F, orc, rng, m, k, n, 3, group)
     y16, _ = _gemm(F, gpu, idx, scales, table, x16, 3, group, workers=workers)
