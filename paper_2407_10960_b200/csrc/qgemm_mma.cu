@@ -284,53 +284,54 @@ void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int work
 //   m <= 32: UPS 2, OCC 1  (64 accumulator floats / lane: one CTA per SM)
 // (A single 16-consumer-warp CTA per SM — CW = 16, OCC = 1 — was measured
 // 10-30 % slower than two 8-warp CTAs on every configs[1] case.)
+// Launch the <BITS, BM, UPS, OCC, CW> instantiation if its shared-memory plan
+// keeps at least `min_stages` pipeline stages.
+template <int BITS, int BM, int UPS, int OCC, int CW>
+bool try_launch(int min_stages, const GemmArgs& a, int m_rows, const void* x, void* y,
+                int workers, long long units, int tiles_k, int gp, int cluster) {
+  if (plan_smem<BITS, BM, UPS, CW>(m_rows, a.group, cluster, smem_cap(OCC)).stages < min_stages)
+    return false;
+  launch_impl<BITS, BM, UPS, OCC, CW>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+  return true;
+}
+
 template <int BITS>
 void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp, int cluster) {
-  // W3 (the 3-bit planes make a unit's stage copy small): larger stages when the
-  // shared-memory plan still keeps >= 3 of them — M <= 8 four units per stage
-  // (measured up to 5 % faster than two), M = 9..16 two (3-4 % faster than
-  // one).  W2 / W4 (the latter's 64 KB vLUT leaves too few stages) keep the
-  // smaller stages; M = 32 keeps two units (one measured 7-10 % slower).
+  // Measured on B200 (profiles/r1/README.md):
+  //  * 4 consumer warps per CTA beat 8 (same CTA count): 5-11 % faster for
+  //    W3 / W4 with M <= 16 — less shared-memory / issue contention per SM
+  //    and half the partial sums to reduce per segment (W2 with M <= 8 is the
+  //    exception: 6 % slower, keeps 8);
+  //  * W3 streams larger stages when >= 3 of them fit: M <= 8 four units per
+  //    stage, 9..16 two, 17..32 two (W2 / W4 keep smaller stages: W2 measured
+  //    slower with four, W4's 64 KB vLUT leaves too few stages);
+  //  * M = 17..32, W2/W3: two CTAs per SM (two 4-warp CTAs fit the register
+  //    file; a launch hands its SM slots to the next one CTA at a time under
+  //    PDL) — 7-11 % faster than one 8-warp CTA; W4 keeps one 8-warp CTA.
+#define FLUTE_TRY(BM, UPS, OCC, CW, MIN) \
+  if (try_launch<BITS, BM, UPS, OCC, CW>(MIN, a, m_rows, x, y, workers, units, tiles_k, gp, cluster)) return
   switch (bm_for(m_rows)) {
     case 8:
-      if constexpr (BITS == 3) {
-        if (plan_smem<BITS, 8, 4, 8>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
-          launch_impl<BITS, 8, 4, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
-          break;
-        }
-      }
-      launch_impl<BITS, 8, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+      if constexpr (BITS == 3) { FLUTE_TRY(8, 4, 2, 4, 3); }
+      if constexpr (BITS == 2) { FLUTE_TRY(8, 2, 2, 8, 2); }  // W2: 8 warps measured 6 % faster
+      FLUTE_TRY(8, 2, 2, 4, 2);
       break;
     case 16:
-      if constexpr (BITS == 3) {
-        if (plan_smem<BITS, 16, 2, 8>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
-          launch_impl<BITS, 16, 2, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
-          break;
-        }
-      }
-      launch_impl<BITS, 16, 1, 2, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+      if constexpr (BITS == 3) { FLUTE_TRY(16, 2, 2, 4, 3); }
+      FLUTE_TRY(16, 1, 2, 4, 2);
       break;
     default:
-      // M = 17..32: W2/W3 run two CTAs per SM with four consumer warps each
-      // (the register budget of two 8-warp CTAs does not fit): a launch's CTAs
-      // then hand their SM slots to the next launch one by one (PDL) instead of
-      // all at once — measured 7-11 % faster than one 8-warp CTA per SM.  W4's
-      // 64 KB vLUT leaves no room for two CTAs' pipelines.
       if constexpr (BITS != 4) {
-        if (plan_smem<BITS, 32, 2, 4>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
-          launch_impl<BITS, 32, 2, 2, 4>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
-          break;
-        }
-        if (plan_smem<BITS, 32, 1, 4>(m_rows, a.group, cluster, smem_cap(2)).stages >= 3) {
-          launch_impl<BITS, 32, 1, 2, 4>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
-          break;
-        }
+        FLUTE_TRY(32, 2, 2, 4, 3);
+        FLUTE_TRY(32, 1, 2, 4, 3);
         // (big cluster receive buffers: the one-CTA-per-SM kernel below)
       }
-      launch_impl<BITS, 32, 2, 1, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+      FLUTE_TRY(32, 2, 1, 8, 2);
       break;
   }
+#undef FLUTE_TRY
+  throw flutesim::InternalError("qgemm: no kernel configuration fits shared memory");
 }
 
 // Cluster split-K (one cluster of C CTAs per 64-column tile, k split C ways,
