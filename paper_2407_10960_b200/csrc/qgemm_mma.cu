@@ -299,13 +299,12 @@ template <int BITS>
 void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
                  long long units, int tiles_k, int gp, int cluster) {
   // Measured on B200 (profiles/r1/README.md):
-  //  * 4 consumer warps per CTA beat 8 (same CTA count): 5-11 % faster for
-  //    W3 / W4 with M <= 16 — less shared-memory / issue contention per SM
-  //    and half the partial sums to reduce per segment (W2 with M <= 8 is the
-  //    exception: 6 % slower, keeps 8);
-  //  * W3 streams larger stages when >= 3 of them fit: M <= 8 four units per
-  //    stage, 9..16 two, 17..32 two (W2 / W4 keep smaller stages: W2 measured
-  //    slower with four, W4's 64 KB vLUT leaves too few stages);
+  //  * 4 consumer warps per CTA beat 8 (same CTA count): 5-11 % faster at
+  //    M <= 16 — less shared-memory / issue contention per SM and half the
+  //    partial sums to reduce per segment;
+  //  * larger stages when >= 3 of them fit: W3 four units per stage for
+  //    M <= 16 (two for 17..32), W2 four for M <= 8 and two for 9..16 (3-8 %
+  //    faster); W4's 64 KB vLUT leaves room for two / one;
   //  * M = 17..32, W2/W3: two CTAs per SM (two 4-warp CTAs fit the register
   //    file; a launch hands its SM slots to the next one CTA at a time under
   //    PDL) — 7-11 % faster than one 8-warp CTA; W4 keeps one 8-warp CTA.
@@ -314,11 +313,15 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
   switch (bm_for(m_rows)) {
     case 8:
       if constexpr (BITS == 3) { FLUTE_TRY(8, 4, 2, 4, 3); }
-      if constexpr (BITS == 2) { FLUTE_TRY(8, 2, 2, 8, 2); }  // W2: 8 warps measured 6 % faster
+      if constexpr (BITS == 2) {
+        FLUTE_TRY(8, 4, 2, 4, 3);
+        FLUTE_TRY(8, 2, 2, 8, 2);  // (two-unit stages: 8 warps measured 6 % faster than 4)
+      }
       FLUTE_TRY(8, 2, 2, 4, 2);
       break;
     case 16:
-      if constexpr (BITS == 3) { FLUTE_TRY(16, 2, 2, 4, 3); }
+      if constexpr (BITS == 3) { FLUTE_TRY(16, 4, 2, 4, 3); }
+      if constexpr (BITS != 4) { FLUTE_TRY(16, 2, 2, 4, 3); }
       FLUTE_TRY(16, 1, 2, 4, 2);
       break;
     default:
