@@ -431,9 +431,9 @@ def run_ours(args):
                          "unit": "GB/s", "frac": round(value / world / peak, 4),
                          "peak_kind": peak_kind,
                          # ncu dram__bytes_read.sum + dram__bytes_write.sum of one
-                         # W3 M=1 4096x14336 launch (profiles/r1/ncu_full_r1i.txt);
+                         # W3 M=1 4096x14336 launch (profiles/r1/ncu_full_r1m.txt);
                          # its algorithmic bytes are 22,974,480 (no re-reads)
-                         "traffic": 23009536,
+                         "traffic": 23003136,
                          "traffic_case": "W3 g128 M=1 K=4096 N=14336, bytes per launch",
                          "kernel": "qgemm_mma_kernel<3,BM> (all 8 launches of a step)"},
             "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
