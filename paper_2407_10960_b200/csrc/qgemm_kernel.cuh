@@ -219,6 +219,13 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
 
   if (threadIdx.x == 0) {
     FLUTE_STAMP(0);
+#ifdef FLUTE_DIAGNOSTICS
+    if (p.dbg) {  // slot 13: the SM this CTA runs on
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.dbg[static_cast<size_t>(blockIdx.x) * 16 + 13] = smid;
+    }
+#endif
     for (int s = 0; s < S; ++s) {
       mbar_init(full(s), 1);
       mbar_init(empty(s), 4);  // one arrive per warp of the stage's quartet

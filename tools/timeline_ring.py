@@ -66,6 +66,11 @@ def main():
                                      col(5, np.max), col(6, np.max)]))
 
 
+    # CTA placement: CTAs per SM of the last launch (diag slot 13 = %smid)
+    sm = res[-1][0].astype(np.int64)[:P, 13]
+    counts = np.bincount(sm, minlength=148)
+    hist = np.bincount(counts)
+    print("CTAs per SM (last launch): " + ", ".join(f"{c} CTAs: {h} SMs" for c, h in enumerate(hist) if h))
     exits = []
     for stamps, _ in res:
         c = stamps.astype(np.int64)[:, 6]
