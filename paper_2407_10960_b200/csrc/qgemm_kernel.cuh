@@ -7,9 +7,10 @@
 // (n-tile major, k inner; streamk.cpp:17-58) with a fixed-order fixup of split
 // tiles (engine.cpp:279-333).
 //
-// One CTA = one Stream-K worker = 8 consumer warps + 1 producer warp + 1
-// epilogue warp, synchronised through mbarriers only (no CTA barrier in the
-// steady state).  Every role walks the CTA's range the same way: tiles
+// One CTA = one Stream-K worker = CW consumer warps (quartets taking stages
+// round-robin; CW = 4 or 8, see launch_bits) + 1 producer warp + 1 epilogue
+// warp, synchronised through mbarriers only (no CTA barrier in the steady
+// state).  Every role walks the CTA's range the same way: tiles
 // (segments) in descending order, and inside a tile stages of UPS units from
 // the top k-slice down, so only a segment's last stage can be short.
 //  * Producer.  Per stage: one 1-D bulk copy (UBLKCP) of the weights (a stage
@@ -18,17 +19,18 @@
 //    copies of the first S stages are issued before the programmatic-
 //    dependent-launch wait, so they overlap the previous kernel in the stream
 //    (OCC = 2 configurations leave room for that CTA to be co-resident).
-//  * Consumer warp w owns k-step w (16 deep) of every unit: LDS of its packed
+//  * Consumer warp q of a quartet owns k-steps 2q, 2q+1 of every unit of the
+//    quartet's stages: LDS of its packed
 //    pair indices, PRMT -> LDS from the 32-way duplicated vLUT, HMUL2 by the
 //    group scale (operand-selector broadcast), mma.sync m16n8k16 with W^T as
 //    the A operand (HMMA.16816.F32), X^T fragments via ldmatrix.  At the end
 //    of a segment it parks its fp32 partial in shared memory and goes on.
-//  * Epilogue warp.  Sums the 8 warp partials in fixed order (deterministic),
-//    then does the Stream-K fixup off the critical path: contributors publish
-//    their fp32 partial and release-add the finisher's flag; finishers
-//    acquire, add contributors in ascending worker (= ascending k) order, add
-//    their own partial, write Y and re-arm their flag (graph / back-to-back
-//    safe).  The descending walk processes a split tile's contributor segment
+//  * Epilogue warp.  Sums the CW warp partials in fixed order (deterministic),
+//    then reduces split tiles off the critical path — cluster split-K through
+//    DSMEM, or Stream-K: contributors publish bit-inverted fp32 partials (an
+//    all-zero slot reads "not written"), finishers poll the data, add
+//    contributors in ascending worker (= ascending k) order to their own
+//    partial, write Y and re-zero the slots (graph / back-to-back safe).  The descending walk processes a split tile's contributor segment
 //    first, so finishers rarely wait.
 #pragma once
 
