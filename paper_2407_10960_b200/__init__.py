@@ -481,6 +481,9 @@ class DeviceWeights:
         m = x.shape[0]
         if y is None:
             y = torch.empty((m, self.n), dtype=torch.float16, device=x.device)
+        elif (y.dtype != torch.float16 or y.device != x.device or tuple(y.shape) != (m, self.n)
+              or not y.is_contiguous()):
+            raise InputError(f"y must be a contiguous float16 [{m}][{self.n}] tensor on {x.device}")
         _check(_lib.flute_gemm(self._h, x.data_ptr(), m, y.data_ptr(), workers,
                                _stream_ptr(stream)))
         return y
@@ -494,6 +497,10 @@ class DeviceWeights:
         if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
             raise InputError(f"x must be a cuda float16 [m][{self.k}] tensor")
         x = x.contiguous()
+        if not 1 <= len(y_ptrs) <= 8 or any(int(p) == 0 for p in y_ptrs):
+            raise InputError("y_ptrs must hold 1..8 non-null device pointers")
+        if ycol0 < 0 or ldy < ycol0 + self.n:
+            raise ConfigError(f"peer output needs ldy >= ycol0 + n ({ycol0} + {self.n})")
         arr = (C.c_void_p * len(y_ptrs))(*[int(p) for p in y_ptrs])
         _check(_lib.flute_gemm_peers(self._h, x.data_ptr(), x.shape[0], arr, len(y_ptrs), ldy,
                                      ycol0, workers, _stream_ptr(stream)))

@@ -747,6 +747,7 @@ int flute_qgemm_peers(const void* x, int m, int k, int n, const void* w, const v
     a.workers = workers;
     a.stream = stream;
     if (n_peers < 1) throw ConfigError("qgemm_peers: need at least one output buffer");
+    flutesim::QuantConfig{bits, group}.validate(k);
     flute_dev::qgemm(a);
   });
 }

@@ -4,6 +4,7 @@
 // flute_dev::qgemm; there is no CPU fallback.
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "device_api.h"
 #include "flutesim/engine.hpp"
@@ -130,6 +131,21 @@ struct DeviceBuffer {
 struct DeviceWeights::Impl {
   int k = 0, n = 0, bits = 0, group = 0;
   DeviceBuffer w, sc, lut, ws, ws_tc, xbuf, ybuf;
+  // Buffers replaced by a larger one.  A HostBatch graph captured earlier may
+  // still point at them, so they are kept until the handle is destroyed (a
+  // handle must outlive its batches) instead of being freed on growth.
+  std::vector<DeviceBuffer> retired;
+
+  // replace `b` by a fresh (zeroed when `zero`) buffer of `bytes`, retiring the old one
+  void regrow(DeviceBuffer& b, std::size_t bytes, bool zero) {
+    DeviceBuffer fresh(bytes);
+    if (zero) {
+      flute_dev::dev_zero(fresh.p, fresh.bytes, nullptr);
+      flute_dev::stream_sync(nullptr);
+    }
+    std::swap(b, fresh);
+    if (fresh.p) retired.push_back(std::move(fresh));
+  }
 
   void upload(const std::vector<std::uint8_t>& packed, const std::vector<std::uint16_t>& scales,
               const std::vector<std::uint32_t>& lut_words) {
@@ -150,11 +166,7 @@ struct DeviceWeights::Impl {
     for (int m = 1; m <= max_m; m = m < 32 ? std::min(32, m * 2) : m + 32)
       need = std::max(need, flute_dev::call_workspace_bytes(m, k, n, 0));
     need = std::max(need, flute_dev::call_workspace_bytes(max_m, k, n, 0));
-    if (need > ws.bytes) {
-      ws = DeviceBuffer(need);
-      flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
-      flute_dev::stream_sync(nullptr);
-    }
+    if (need > ws.bytes) regrow(ws, need, true);
     for (int m = 64; m <= max_m; m = m < 512 ? m * 2 : m + 512) grow_tc(m);
     grow_tc(max_m);
   }
@@ -163,7 +175,7 @@ struct DeviceWeights::Impl {
   // Stream-K slots in `ws` are never touched by M >= 64 calls
   void grow_tc(int m) {
     const std::size_t need = flute_dev::tc_call_part_bytes(m, k, n);
-    if (need > ws_tc.bytes) ws_tc = DeviceBuffer(need);
+    if (need > ws_tc.bytes) regrow(ws_tc, need, false);
   }
 
   // autotuned decomposition per m-class (row block 8 / 16 / 32), -1 = none
@@ -175,11 +187,7 @@ struct DeviceWeights::Impl {
   // never inside CUDA-graph capture)
   void ensure_ws(int m, int workers) {
     const std::size_t need = flute_dev::call_workspace_bytes(m, k, n, workers);
-    if (need > ws.bytes) {
-      ws = DeviceBuffer(need);
-      flute_dev::dev_zero(ws.p, ws.bytes, nullptr);
-      flute_dev::stream_sync(nullptr);
-    }
+    if (need > ws.bytes) regrow(ws, need, true);
     grow_tc(m);
   }
 
@@ -326,11 +334,7 @@ std::string DeviceWeights::autotune(int m, void* stream, int reps) {
   for (const flute_dev::Decomp& c : cands) {  // grow the workspace before timing
     if (c.cluster == 0) {
       const std::size_t need = flute_dev::workspace_bytes(m, c.workers);
-      if (need > im.ws.bytes) {
-        im.ws = DeviceBuffer(need);
-        flute_dev::dev_zero(im.ws.p, im.ws.bytes, nullptr);
-        flute_dev::stream_sync(nullptr);
-      }
+      if (need > im.ws.bytes) im.regrow(im.ws, need, true);
     }
   }
   double best_t = 1e30;
@@ -375,8 +379,8 @@ void DeviceWeights::gemm_host_raw(const std::uint16_t* x_host, int m, std::uint1
   if (m < 1) throw ConfigError("gemm_host: m must be >= 1");
   const std::size_t xb = static_cast<std::size_t>(m) * impl_->k * 2;
   const std::size_t yb = static_cast<std::size_t>(m) * impl_->n * 2;
-  if (impl_->xbuf.bytes < xb) impl_->xbuf = DeviceBuffer(xb);
-  if (impl_->ybuf.bytes < yb) impl_->ybuf = DeviceBuffer(yb);
+  if (impl_->xbuf.bytes < xb) impl_->regrow(impl_->xbuf, xb, false);
+  if (impl_->ybuf.bytes < yb) impl_->regrow(impl_->ybuf, yb, false);
   flute_dev::h2d(impl_->xbuf.p, x_host, xb, stream);
   impl_->gemm(impl_->xbuf.p, m, impl_->ybuf.p, workers, stream);
   flute_dev::d2h(y_host, impl_->ybuf.p, yb, stream);

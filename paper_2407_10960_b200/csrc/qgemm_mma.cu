@@ -460,6 +460,13 @@ size_t call_workspace_bytes(int m, int k, int n, int workers) {
 void qgemm(const GemmArgs& a) {
   if (a.m < 1) throw flutesim::ConfigError("qgemm: m must be >= 1");
   if (a.bits < 2 || a.bits > 4) throw flutesim::ConfigError("qgemm: bits must be 2, 3 or 4");
+  // every entry point (flute_qgemm, flute_qgemm_peers, handles) lands here:
+  // the group must be a power of two in [32, 256] (the kernel shifts by
+  // log2(group)) — a zero or odd group would otherwise divide by zero or pick
+  // the wrong scales
+  if (a.group < 32 || a.group > 256 || (a.group & (a.group - 1)) != 0)
+    throw flutesim::ConfigError("qgemm: group must be a power of two in [32, 256], got " +
+                                std::to_string(a.group));
   if (a.k % 16 != 0 || a.n % 16 != 0 || a.k < 16 || a.n < 16)
     throw flutesim::ConfigError("qgemm: k and n must be positive multiples of 16");
   if (!a.x || !a.w || !a.scales || !a.vlut || !a.workspace || (a.n_peers == 0 && !a.y))

@@ -107,7 +107,11 @@ class ShardedWeights:
 
     def gemm_peer(self, x, workers: int = 0):
         """Fused all-gather: the epilogue writes this rank's columns into every
-        rank's symmetric Y buffer; one barrier makes the full Y visible."""
+        rank's symmetric Y buffer; one barrier makes the full Y visible.
+
+        The returned tensor ALIASES the internal symmetric buffer for this m:
+        it is valid until the next gemm_peer call with the same m (which
+        overwrites it).  Copy it (``.clone()``) to keep a result."""
         t, h = self._symm_buffer(x.shape[0])
         ptrs = [int(p) for p in h.buffer_ptrs]
         h.barrier()  # every rank done reading the previous contents
