@@ -12,10 +12,9 @@
 // reference rule — equals the RNE f16x2 product bit for bit (subnormals are
 // kept by f16 arithmetic on sm_100).
 //
-// Per lane slot, the device layout (host_pack.cpp) gives one word of 16 pair
-// indices q = 4c + p (c = k-step within the slot's quad of k-steps, p =
-// A-fragment register):
-//   4-bit: uint4, byte p of word c = pair 4c+p                      (8 bits/pair)
+// Per lane and 16-deep k step, the device layout (host_pack.cpp) gives 16 pair
+// indices q = 4j + p (atom j = 16-column block, p = A-fragment register):
+//   4-bit: uint4, byte p of word j = pair 4j+p                      (8 bits/pair)
 //   2-bit: uint2, word h: low nibbles of bytes 0..3 = pairs 8h+0..3, high
 //          nibbles = pairs 8h+4..7                                   (4 bits/pair)
 //   3-bit: same nibble layout for the hi plane (hi_k<<2 | hi_k1), plus one u32
@@ -45,27 +44,27 @@ struct LaneBits<3> {
   uint32_t lo;
 };
 
-// Byte vector of the 4 device pair indices of component j (byte p = register p).
+// Byte vector of the 4 device pair indices of atom j (byte p = register p).
 template <int BITS>
-__device__ __forceinline__ uint32_t word_index_bytes(const LaneBits<BITS>& lb, int j);
+__device__ __forceinline__ uint32_t atom_index_bytes(const LaneBits<BITS>& lb, int j);
 
 template <>
-__device__ __forceinline__ uint32_t word_index_bytes<4>(const LaneBits<4>& lb, int j) {
+__device__ __forceinline__ uint32_t atom_index_bytes<4>(const LaneBits<4>& lb, int j) {
   return j == 0 ? lb.w.x : j == 1 ? lb.w.y : j == 2 ? lb.w.z : lb.w.w;
 }
 template <>
-__device__ __forceinline__ uint32_t word_index_bytes<2>(const LaneBits<2>& lb, int j) {
+__device__ __forceinline__ uint32_t atom_index_bytes<2>(const LaneBits<2>& lb, int j) {
   const uint32_t w = (j >> 1) ? lb.w.y : lb.w.x;
   return (j & 1) ? ((w >> 4) & 0x0F0F0F0Fu) : (w & 0x0F0F0F0Fu);
 }
 template <>
-__device__ __forceinline__ uint32_t word_index_bytes<3>(const LaneBits<3>& lb, int j) {
+__device__ __forceinline__ uint32_t atom_index_bytes<3>(const LaneBits<3>& lb, int j) {
   const uint32_t w = (j >> 1) ? lb.hi.y : lb.hi.x;
   const uint32_t hi = (j & 1) ? ((w >> 2) & 0x3C3C3C3Cu) : ((w << 2) & 0x3C3C3C3Cu);
   return hi | ((lb.lo >> (2 * j)) & 0x03030303u);
 }
 
-// The four A-fragment registers of one component: a[p] = vLUT[idx_p] * (s, s), with
+// The four A-fragment registers of atom j: a[p] = vLUT[idx_p] * (s, s), with
 // regs 0/2 (column g) scaled by the low half of `scales` and regs 1/3 (column
 // g+8) by the high half.  The half broadcast folds into the HMUL2 operand
 // selector (.H0_H0 / .H1_H1), so it costs no instruction.

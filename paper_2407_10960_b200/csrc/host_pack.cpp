@@ -4,27 +4,22 @@
 //
 // Device layout.  The weight stream is a sequence of Stream-K
 // units u = nt * tiles_k + kt (n-tile major, k inner — the reference's unit
-// order), each covering 64 output columns x 128 k = 4 column blocks ("atoms",
-// 16 columns) x 8 k-steps (16 deep).  Per (atom j, k-step s) a lane owns the
-// eight weights of a 16x16 MMA A-fragment (rows = n, cols = k, g = lane/4,
-// t = lane%4):
+// order), each covering 64 output columns x 128 k.  Inside a unit, the eight
+// consumer warps w own one 16-deep k step each; every lane owns, per 16x16
+// "atom" j (columns 16j..16j+15), the eight weights the swapped
+// mma.m16n8k16 A-fragment needs (rows = n, cols = k, g = lane/4, t = lane%4):
 //     reg p=0: n=g,   k=2t,2t+1     reg p=1: n=g+8, k=2t,2t+1
 //     reg p=2: n=g,   k=2t+8,+9     reg p=3: n=g+8, k=2t+8,+9
-// — exactly the thread -> (TMEM lane, column) pattern of tcgen05.st.16x128b,
-// so the dequantised registers go to tensor memory unchanged (A operand of
-// the tcgen05 "TS" MMA, qgemm_ts.cuh).  Lane words are ordered
-//     slot = (quad * 4 + j) * 32 + lane,   quad = s / 4,   c = s % 4
-// so one word holds FOUR CONSECUTIVE k-steps of ONE atom (the rows a warp may
-// write in tensor memory are fixed by its warp id), and the two k-quads of a
-// unit are contiguous halves.  Each (n, k, k+1) pair is one vLUT index, first
-// (even k) in the high bits; component c of the word (k-step 4*quad + c):
-//   4-bit: byte p of 32-bit word c = idx_k << 4 | idx_k1 (16 B per slot);
-//   2-bit: word c>>1, byte p, nibble c&1 = idx_k << 2 | idx_k1 (8 B per slot);
+// Each (n, k, k+1) pair is stored as one vLUT index, first (even k) in the high
+// bits, pair q = 4j + p of the lane:
+//   4-bit: byte p of word j = idx_k << 4 | idx_k1 (a lane's 4 atoms are one
+//          16-byte LDS);
+//   2-bit: word j>>1, byte p, nibble j&1 = idx_k << 2 | idx_k1 (8 B per lane);
 //   3-bit: a 2-bit plane laid out like 2-bit with nibble hi_k << 2 | hi_k1
-//          (8 B per slot, the unit's first 2 KiB) and a 1-bit plane whose byte
-//          p holds lo_k << 1 | lo_k1 at bits 2c..2c+1 (4 B per slot, last
-//          1 KiB); the device vLUT is permuted to index (hi_pair << 2) | lo_pair.
-// These are exactly the byte vectors dequant.cuh's word_index_bytes expects.
+//          (8 B per lane, the unit's first 2 KiB) and a 1-bit plane whose byte p
+//          holds lo_k << 1 | lo_k1 at bits 2j..2j+1 (4 B per lane, last 1 KiB);
+//          the device vLUT is permuted to index (hi_pair << 2) | lo_pair.
+// These are exactly the byte vectors dequant.cuh's atom_index_bytes expects.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -189,8 +184,8 @@ DeviceGeometry device_geometry(int k, int n, int bits, int group) {
 
 namespace {
 
-// Visits every (unit, slot, component, reg) position of the device stream
-// with the (row k, column n) coordinate of the pair's first weight.
+// Visits every (unit, warp, lane, atom, reg) slot of the device stream and the
+// (n, k) coordinate of the pair's first weight.
 template <class F>
 void for_each_pair_slot(const DeviceGeometry& g, F&& f) {
   const long units = g.units();
@@ -198,14 +193,15 @@ void for_each_pair_slot(const DeviceGeometry& g, F&& f) {
   for (long u = 0; u < units; ++u) {
     const int nt = static_cast<int>(u / g.tiles_k());
     const int kt = static_cast<int>(u % g.tiles_k());
-    for (int slot = 0; slot < 256; ++slot) {
-      const int quad = slot >> 7, j = (slot >> 5) & 3, lane = slot & 31;
-      const int gr = lane >> 2, t = lane & 3;
-      for (int c = 0; c < 4; ++c) {
-        for (int p = 0; p < 4; ++p) {
-          const int col = nt * kUnitN + 16 * j + gr + 8 * (p & 1);
-          const int row = kt * kUnitK + 16 * (4 * quad + c) + 2 * t + 8 * (p >> 1);
-          f(u, slot, c, p, row, col);
+    for (int w = 0; w < 8; ++w) {
+      for (int lane = 0; lane < 32; ++lane) {
+        const int gr = lane >> 2, t = lane & 3;
+        for (int j = 0; j < 4; ++j) {
+          for (int p = 0; p < 4; ++p) {
+            const int col = nt * kUnitN + 16 * j + gr + 8 * (p & 1);
+            const int row = kt * kUnitK + 16 * w + 2 * t + 8 * (p >> 1);
+            f(u, w, lane, j, p, row, col);
+          }
         }
       }
     }
@@ -230,9 +226,10 @@ std::vector<std::uint8_t> pack_device(const std::vector<std::uint8_t>& indices, 
   };
   std::vector<std::uint8_t> out(g.weight_bytes(), 0);
   const std::size_t ub = g.unit_bytes();
-  for_each_pair_slot(g, [&](long u, int slot, int j, int p, int row, int col) {
+  for_each_pair_slot(g, [&](long u, int w, int lane, int j, int p, int row, int col) {
     std::uint8_t* unit = out.data() + static_cast<std::size_t>(u) * ub;
     const std::uint32_t a = at(row, col), b = at(row + 1, col);
+    const int slot = w * 32 + lane;
     if (bits == 4) {
       unit[slot * 16 + j * 4 + p] = static_cast<std::uint8_t>((a << 4) | b);
     } else if (bits == 2) {
@@ -258,9 +255,10 @@ std::vector<std::uint8_t> unpack_device(const std::vector<std::uint8_t>& dev, in
   if (dev.size() != g.weight_bytes()) throw InputError("unpack_device: size mismatch");
   std::vector<std::uint8_t> out(static_cast<std::size_t>(k) * n, 0);
   const std::size_t ub = g.unit_bytes();
-  for_each_pair_slot(g, [&](long u, int slot, int j, int p, int row, int col) {
+  for_each_pair_slot(g, [&](long u, int w, int lane, int j, int p, int row, int col) {
     if (row >= k || col >= n) return;
     const std::uint8_t* unit = dev.data() + static_cast<std::size_t>(u) * ub;
+    const int slot = w * 32 + lane;
     std::uint32_t a = 0, b = 0;
     if (bits == 4) {
       const std::uint32_t v = unit[slot * 16 + j * 4 + p];

@@ -112,8 +112,8 @@ __global__ void pack_device_kernel(const uint8_t* __restrict__ idx, int k, int n
   const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= units * 256) return;
   const long u = t >> 8;
-  const int slot = static_cast<int>(t & 255);  // (quad * 4 + atom) * 32 + lane
-  const int quad = slot >> 7, atom = (slot >> 5) & 3, lane = slot & 31;
+  const int slot = static_cast<int>(t & 255);
+  const int w = slot >> 5, lane = slot & 31;
   const int nt = static_cast<int>(u / tiles_k), kt = static_cast<int>(u % tiles_k);
   const int gr = lane >> 2, tq = lane & 3;
   const uint32_t zero = (1u << (bits - 1)) - 1u;
@@ -128,9 +128,8 @@ __global__ void pack_device_kernel(const uint8_t* __restrict__ idx, int k, int n
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      // component j of the slot = k-step 4 * quad + j of column block `atom`
-      const int col = nt * kUnitN + 16 * atom + gr + 8 * (p & 1);
-      const int row = kt * kUnitK + 16 * (4 * quad + j) + 2 * tq + 8 * (p >> 1);
+      const int col = nt * kUnitN + 16 * j + gr + 8 * (p & 1);
+      const int row = kt * kUnitK + 16 * w + 2 * tq + 8 * (p >> 1);
       const uint32_t a = at(row, col), b = at(row + 1, col);
       if (bits == 4) {
         bytes[j * 4 + p] = static_cast<uint8_t>((a << 4) | b);

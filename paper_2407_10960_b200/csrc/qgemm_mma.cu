@@ -1,8 +1,6 @@
-// flute-b200 — host side of the LUT-GEMM: the launcher of the memory-bound
-// tcgen05 "TS" kernel (qgemm_ts.cuh, M <= 64 rows per launch), the dispatch
-// between it and the compute-bound kernel (qgemm_tc.cu), the device
-// self-check kernels (exhaustive dequant, tensor-core mma_fragment), host
-// batches and small CUDA runtime helpers.
+// flute-b200 — host launcher of the memory-bound LUT-GEMM (kernel in
+// qgemm_kernel.cuh) plus the device self-check kernels (exhaustive dequant,
+// tensor-core mma_fragment) and small CUDA runtime helpers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -15,13 +13,9 @@
 #include "device_api.h"
 #include "flutesim/errors.hpp"
 #include "ptx.cuh"
-#include "qgemm_ts.cuh"
+#include "qgemm_kernel.cuh"
 
 namespace flute_dev {
-
-using ts::kMaxPeers;
-using ts::kUnitK;
-using ts::kUnitN;
 
 // ---------------------------------------------------------------------------
 // host side
@@ -112,66 +106,106 @@ const DevProps& props() {
   return pr;
 }
 
-// X rows per TS launch (UMMA N): 8 / 16 / 32 / 64.
-int nb_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : m <= 32 ? 32 : 64; }
+// FLUTE_DEBUG_TIMES=1 (diag build): per-CTA %globaltimer stamps {start,
+// producer issued, LUT ready, first stage ready, segment end, last segment
+// end, exit, finisher acquired} followed by a per-stage trace of consumer
+// warp 0: 64 stages x {wait begin, data ready, compute done}.
+constexpr size_t kDbgPerCta = 16 + 64 * 3;
+unsigned long long* g_dbg = nullptr;
+int g_dbg_cap = 0;       // CTAs per slot
+int g_dbg_slots = 1;     // FLUTE_DEBUG_TIMES=N: ring of N launches (no per-launch memset,
+int g_dbg_next = 0;      // so programmatic-dependent launches still overlap)
+unsigned long long* debug_times_buffer(int workers) {
+  static const char* env = std::getenv("FLUTE_DEBUG_TIMES");
+  if (!env) return nullptr;
+  const int slots = std::max(1, std::atoi(env));
+  const size_t slot_words = static_cast<size_t>(workers) * kDbgPerCta;
+  if (g_dbg_cap < workers || g_dbg_slots != slots) {
+    if (g_dbg) cudaFree(g_dbg);
+    FLUTE_CUDA(cudaMalloc(&g_dbg, slot_words * slots * 8));
+    FLUTE_CUDA(cudaMemset(g_dbg, 0, slot_words * slots * 8));
+    g_dbg_cap = workers;
+    g_dbg_slots = slots;
+    g_dbg_next = 0;
+  }
+  if (slots == 1) FLUTE_CUDA(cudaMemset(g_dbg, 0, slot_words * 8));
+  unsigned long long* b = g_dbg + static_cast<size_t>(g_dbg_next) * g_dbg_cap * kDbgPerCta;
+  g_dbg_next = (g_dbg_next + 1) % slots;
+  return b;
+}
+
+int bm_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : 32; }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-size_t smem_optin() { return props().smem_optin; }
+// Shared memory available to one CTA when `occ` CTAs must fit on an SM.
+size_t smem_cap(int occ) {
+  static thread_local int dev_cached = -1;
+  static thread_local size_t per_sm = 0, reserved = 0, optin = 0;
+  int dev = 0;
+  FLUTE_CUDA(cudaGetDevice(&dev));
+  if (dev != dev_cached) {
+    int v = 0;
+    FLUTE_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    per_sm = static_cast<size_t>(v);
+    FLUTE_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    reserved = static_cast<size_t>(v);
+    optin = props().smem_optin;
+    dev_cached = dev;
+  }
+  return std::min(optin, per_sm / static_cast<size_t>(occ) - reserved);
+}
 
-struct TsPlan {
-  int stages = 0, ups = 1;
-  uint32_t bar_off = 0, recv_off = 0, stage_off = 0, stage_bytes = 0, x_bytes = 0, w_bytes = 0;
+struct SmemPlan {
+  uint32_t part_off = 0, part_stride = 0, stage_off = 0, stage_bytes = 0, x_bytes = 0, bar_off = 0;
+  uint32_t recv_off = 0;
+  int stages = 0;
   size_t total = 0;
 };
 
-// [vLUT | barriers + misc | cluster receive buffer | stages...],
-// stage = [X (ups units x 2 chunks x NB rows x 128 B) | weights | scales].
-TsPlan plan_ts(int bits, int nb, int group, int cluster, int ups, size_t cap) {
-  TsPlan pl;
-  pl.ups = ups;
-  size_t off = static_cast<size_t>(1u << (2 * bits)) * kLutRowBytes;
+// [vLUT (+ partial rows in its row gaps) | partials | barriers | stages...],
+// stage = [X (1024-aligned, zero row last) | weights | scales].
+template <int BITS, int BM, int UPS, int CW>
+SmemPlan plan_smem(int m, int group, int cluster, size_t cap) {
+  using Cf = Cfg<BITS, BM, UPS, CW>;
+  SmemPlan pl;
+  size_t off = Cf::kLutBytes;
+  pl.part_off = static_cast<uint32_t>(off);
+  pl.part_stride = 128;
+  off += Cf::kPartBytes;
+  pl.recv_off = static_cast<uint32_t>(off);  // cluster split-K receive buffer
+  if (cluster > 1) off += static_cast<size_t>(cluster - 1) * Cf::kFrag * 128;
   pl.bar_off = static_cast<uint32_t>(off);
-  off += 8 * (5 * ts::kMaxStages + 6) + 16;
-  off = align_up(off, 128);
-  pl.recv_off = static_cast<uint32_t>(off);
-  if (cluster > 1) off += static_cast<size_t>(cluster - 1) * nb * 64 * 4;
-  off = align_up(off, 1024);
+  off = align_up(off + Cf::kBarBytes, 1024);
   pl.stage_off = static_cast<uint32_t>(off);
-  pl.x_bytes = static_cast<uint32_t>(2 * ups * nb * 128);
-  pl.w_bytes = static_cast<uint32_t>(ups * bits * 1024);
-  const int ng = ups * std::max(1, kUnitK / group) + 1;
-  pl.stage_bytes = static_cast<uint32_t>(align_up(pl.x_bytes + pl.w_bytes + static_cast<size_t>(ng) * 128, 1024));
+  pl.x_bytes = static_cast<uint32_t>(align_up(2 * UPS * m * 128 + (m < BM ? 128 : 0), 1024));
+  const int ng = UPS * std::max(1, kUnitK / group);
+  pl.stage_bytes =
+      static_cast<uint32_t>(align_up(pl.x_bytes + Cf::kWBytes + static_cast<size_t>(ng) * 128, 1024));
   const long fit = cap > off ? static_cast<long>((cap - off) / pl.stage_bytes) : 0;
-  pl.stages = static_cast<int>(std::min<long>(ts::kMaxStages, fit));
+  pl.stages = static_cast<int>(std::min<long>(kMaxStages, fit));
   pl.total = off + static_cast<size_t>(pl.stages) * pl.stage_bytes;
   return pl;
 }
 
-// dequant warps per CTA (multiple of 4: each TMEM subpartition gets DW/4)
-constexpr int kTsDw = 12;
-
-template <int BITS, int NB>
-void launch_ts(const GemmArgs& a, int m_rows, const void* x, void* y, int workers, long long units,
-               int tiles_k, int gp, int cluster) {
+template <int BITS, int BM, int UPS, int OCC, int CW>
+void launch_impl(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
+                 long long units, int tiles_k, int gp, int cluster) {
+  using Cf = Cfg<BITS, BM, UPS, CW>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   FLUTE_CUDA(cudaGetDevice(&dev));
-  // units per stage: two (fewer, larger copies) while the X part stays small
-  int ups = NB <= 16 ? 2 : 1;
-  if (const char* e = std::getenv("FLUTE_TS_UPS")) ups = std::max(1, std::min(4, std::atoi(e)));
-  TsPlan pl = plan_ts(BITS, NB, a.group, cluster, ups, smem_optin());
-  if (pl.stages < 2 && ups > 1) pl = plan_ts(BITS, NB, a.group, cluster, 1, smem_optin());
+  const SmemPlan pl = plan_smem<BITS, BM, UPS, CW>(m_rows, a.group, cluster, smem_cap(OCC));
   if (pl.stages < 2) throw flutesim::InternalError("qgemm: shared-memory plan has < 2 stages");
-  auto kern = ts::qgemm_ts_kernel<BITS, NB, kTsDw>;
+  auto kern = qgemm_mma_kernel<BITS, BM, UPS, OCC, CW>;
   if (configured_dev != dev) {
     FLUTE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem_optin())));
+                                    static_cast<int>(smem_cap(OCC))));
     configured_dev = dev;
   }
   const bool x3d = a.k % 64 == 0 && std::getenv("FLUTE_X2D") == nullptr;
-  const CUtensorMap map = make_x_map(x, m_rows, a.k, NB, 2 * pl.ups, x3d);
-  ts::Params kp{};
+  const CUtensorMap map = make_x_map(x, m_rows, a.k, m_rows, 2 * UPS, x3d);
+  KParams kp{};
   kp.w = static_cast<const uint8_t*>(a.w);
   kp.sc = static_cast<const uint8_t*>(a.scales);
   kp.vlut = static_cast<const uint32_t*>(a.vlut);
@@ -202,20 +236,26 @@ void launch_ts(const GemmArgs& a, int m_rows, const void* x, void* y, int worker
   kp.units = static_cast<int>(units);
   kp.workers = workers;
   kp.stages = pl.stages;
-  kp.ups = pl.ups;
-  kp.use_ticket = cluster <= 1 && workers > props().sms ? 1 : 0;
-  kp.x3d = x3d ? 1 : 0;
+  kp.use_ticket = cluster <= 1 && workers > props().sms * OCC ? 1 : 0;
   kp.cluster = cluster;
-  kp.bar_off = pl.bar_off;
   kp.recv_off = pl.recv_off;
+  kp.x3d = x3d ? 1 : 0;
+  kp.part_off = pl.part_off;
+  kp.part_stride = pl.part_stride;
   kp.stage_off = pl.stage_off;
   kp.stage_bytes = pl.stage_bytes;
   kp.x_bytes = pl.x_bytes;
-  kp.w_bytes = pl.w_bytes;
+  kp.bar_off = pl.bar_off;
+  {
+    static const char* d = std::getenv("FLUTE_DIAG");
+    kp.diag = d ? std::atoi(d) : 0;
+  }
+  kp.dbg = debug_times_buffer(workers);
+  (void)Cf::kWBytes;
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(workers));
-  cfg.blockDim = dim3(ts::threads_for(kTsDw));
+  cfg.blockDim = dim3(threads_for(CW));
   cfg.dynamicSmemBytes = pl.total;
   cfg.stream = static_cast<cudaStream_t>(a.stream);
   cudaLaunchAttribute attr[2];
@@ -238,27 +278,80 @@ void launch_ts(const GemmArgs& a, int m_rows, const void* x, void* y, int worker
   FLUTE_CUDA(cudaLaunchKernelEx(&cfg, kern, map, kp));
 }
 
+// Per row-block: (stage depth UPS units, CTAs per SM the kernel is built for).
+//   m <= 8 : UPS 2, OCC 2  (co-resident with the next launch)
+//   m <= 16: UPS 1, OCC 2
+//   m <= 32: UPS 2, OCC 1  (64 accumulator floats / lane: one CTA per SM)
+// (A single 16-consumer-warp CTA per SM — CW = 16, OCC = 1 — was measured
+// 10-30 % slower than two 8-warp CTAs on every configs[1] case.)
+// Launch the <BITS, BM, UPS, OCC, CW> instantiation if its shared-memory plan
+// keeps at least `min_stages` pipeline stages.
+template <int BITS, int BM, int UPS, int OCC, int CW>
+bool try_launch(int min_stages, const GemmArgs& a, int m_rows, const void* x, void* y,
+                int workers, long long units, int tiles_k, int gp, int cluster) {
+  if (plan_smem<BITS, BM, UPS, CW>(m_rows, a.group, cluster, smem_cap(OCC)).stages < min_stages)
+    return false;
+  launch_impl<BITS, BM, UPS, OCC, CW>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster);
+  return true;
+}
+
 template <int BITS>
-void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers, long long units,
-                 int tiles_k, int gp, int cluster) {
-  switch (nb_for(m_rows)) {
-    case 8: launch_ts<BITS, 8>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
-    case 16: launch_ts<BITS, 16>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
-    case 32: launch_ts<BITS, 32>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
-    default: launch_ts<BITS, 64>(a, m_rows, x, y, workers, units, tiles_k, gp, cluster); break;
+void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int workers,
+                 long long units, int tiles_k, int gp, int cluster) {
+  // Measured on B200 (profiles/r1/README.md):
+  //  * 4 consumer warps per CTA beat 8 (same CTA count): 5-11 % faster at
+  //    M <= 16 — less shared-memory / issue contention per SM and half the
+  //    partial sums to reduce per segment;
+  //  * larger stages when >= 3 of them fit: W3 four units per stage for
+  //    M <= 16 (two for 17..32), W2 four for M <= 8 and two for 9..16 (3-8 %
+  //    faster); W4's 64 KB vLUT leaves room for two / one;
+  //  * M = 17..32, W2/W3: two CTAs per SM (two 4-warp CTAs fit the register
+  //    file; a launch hands its SM slots to the next one CTA at a time under
+  //    PDL) — 7-11 % faster than one 8-warp CTA; W4 keeps one 8-warp CTA.
+#define FLUTE_TRY(BM, UPS, OCC, CW, MIN) \
+  if (try_launch<BITS, BM, UPS, OCC, CW>(MIN, a, m_rows, x, y, workers, units, tiles_k, gp, cluster)) return
+  switch (bm_for(m_rows)) {
+    case 8:
+      if constexpr (BITS == 3) { FLUTE_TRY(8, 4, 2, 4, 3); }
+      if constexpr (BITS == 2) {
+        FLUTE_TRY(8, 4, 2, 4, 3);
+        FLUTE_TRY(8, 2, 2, 8, 2);  // (two-unit stages: 8 warps measured 6 % faster than 4)
+      }
+      FLUTE_TRY(8, 2, 2, 4, 2);
+      break;
+    case 16:
+      if constexpr (BITS == 3) { FLUTE_TRY(16, 4, 2, 4, 3); }
+      if constexpr (BITS != 4) { FLUTE_TRY(16, 2, 2, 4, 3); }
+      FLUTE_TRY(16, 1, 2, 4, 2);
+      break;
+    default:
+      if constexpr (BITS != 4) {
+        FLUTE_TRY(32, 2, 2, 4, 3);
+        FLUTE_TRY(32, 1, 2, 4, 3);
+        // (big cluster receive buffers: the one-CTA-per-SM kernel below)
+      }
+      FLUTE_TRY(32, 2, 1, 8, 2);
+      break;
   }
+#undef FLUTE_TRY
+  throw flutesim::InternalError("qgemm: no kernel configuration fits shared memory");
 }
 
 // Cluster split-K (one cluster of C CTAs per 64-column tile, k split C ways,
 // DSMEM reduction) when the tile count T fills >= 3/4 of the SMs with
-// T*C <= #SMs (one CTA per SM); returns C (1 = no split), or 0 for Stream-K.
-int cluster_for(long long tiles_n, int tiles_k) {
+// T*C <= #SMs; returns C (1 = no split), or 0 for Stream-K.
+// CTAs per SM the kernel for an m-row launch is built for (launch_bits).
+int occ_for(int m, int bits) { return bm_for(std::min(m, 32)) <= 16 || bits != 4 ? 2 : 1; }
+
+int cluster_for(long long tiles_n, int tiles_k, int m, int bits) {
   if (std::getenv("FLUTE_NO_CLUSTER")) return 0;
   if (const char* f = std::getenv("FLUTE_FORCE_CLUSTER")) {  // tests: force cluster size C
     const int c = std::atoi(f);
     if (c >= 1 && c <= 8 && c <= tiles_k) return c;
   }
-  const int sms = props().sms;
+  // capacity: all co-resident CTA slots (two per SM for the OCC = 2 kernels,
+  // measured faster than leaving the second slot to the next launch)
+  const int sms = props().sms * occ_for(m, bits);
   for (int c = 8; c >= 1; c /= 2) {
     if (c > tiles_k) continue;
     const long long g = tiles_n * c;
@@ -282,9 +375,7 @@ int sm_count(int device) {
 }
 
 int max_workers(int m, int bits) {
-  (void)m;
-  (void)bits;
-  return props().sms;  // co-resident CTA slots (one TS CTA per SM)
+  return props().sms * occ_for(m, bits);  // co-resident CTA slots
 }
 
 int default_workers(int m, int k, int n, int bits) {
@@ -292,22 +383,27 @@ int default_workers(int m, int k, int n, int bits) {
   (void)bits;
   const int tiles_k = (k + kUnitK - 1) / kUnitK;
   const long long tiles_n = (n + kUnitN - 1) / kUnitN;
-  const int c = cluster_for(tiles_n, tiles_k);
+  const int c = cluster_for(tiles_n, tiles_k, m, bits);
   if (c > 0) return static_cast<int>(tiles_n * c);
-  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, props().sms));
+  return static_cast<int>(std::min<long long>(tiles_k * tiles_n, max_workers(m, bits)));
 }
 
 void debug_times(unsigned long long* out, int workers) {
-  (void)out;
-  (void)workers;
-  throw flutesim::InputError("debug_times: per-CTA timelines are not built into this kernel");
+  if (!g_dbg) throw flutesim::InputError("FLUTE_DEBUG_TIMES not enabled");
+  // slot i (launch i of the ring) at out + i * workers * kDbgPerCta
+  FLUTE_CUDA(cudaDeviceSynchronize());
+  for (int i = 0; i < g_dbg_slots; ++i)
+    FLUTE_CUDA(cudaMemcpy(out + static_cast<size_t>(i) * workers * kDbgPerCta,
+                          g_dbg + static_cast<size_t>(i) * g_dbg_cap * kDbgPerCta,
+                          static_cast<size_t>(std::min(workers, g_dbg_cap)) * kDbgPerCta * 8,
+                          cudaMemcpyDeviceToHost));
 }
 
 size_t workspace_bytes(int m, int workers) {
-  const int nb = nb_for(std::min(m, 64));
+  const int bm = bm_for(std::min(m, 32));
   const size_t flag_bytes = (static_cast<size_t>(workers) + 2) * 4;
   const size_t flag_span = (flag_bytes + 255) / 256 * 256;
-  return flag_span + static_cast<size_t>(workers) * nb * 64 * 4;  // [worker][nb][64] fp32
+  return flag_span + static_cast<size_t>(workers) * (bm / 8) * 16 * 32 * 4;
 }
 
 double time_launches(const std::function<void()>& fn, int reps, void* stream) {
@@ -342,7 +438,7 @@ std::vector<Decomp> decomp_candidates(int m, int k, int n, int bits) {
   std::vector<Decomp> out;
   const int tiles_k = (k + kUnitK - 1) / kUnitK;
   const long long tiles_n = (n + kUnitN - 1) / kUnitN;
-  const int slots = max_workers(std::min(m, 64), bits);
+  const int slots = max_workers(std::min(m, 32), bits);
   out.push_back({-1, 0});  // the heuristic's own choice
   for (int c = 1; c <= 8; c *= 2)
     if (c <= tiles_k && tiles_n * c <= slots && 2 * tiles_n * c >= slots) out.push_back({c, 0});
@@ -357,7 +453,7 @@ size_t tc_call_part_bytes(int m, int k, int n) {
 
 size_t call_workspace_bytes(int m, int k, int n, int workers) {
   // (sized for the larger co-residency of any bit width)
-  const size_t mma = workspace_bytes(std::min(m, 64), workers > 0 ? workers : max_workers(std::min(m, 64), 3) * 4);
+  const size_t mma = workspace_bytes(std::min(m, 32), workers > 0 ? workers : max_workers(std::min(m, 32), 3) * 4);
   return tc_enabled(m) ? std::max(mma, tc_workspace_bytes(m, k, n, props().sms)) : mma;
 }
 
@@ -393,7 +489,7 @@ void qgemm(const GemmArgs& a) {
   int cluster = a.cluster >= 1   ? std::min(a.cluster, tiles_k)
                 : a.cluster == 0 ? 0
                 : a.workers > 0  ? 0
-                                 : cluster_for(np / kUnitN, tiles_k);
+                                 : cluster_for(np / kUnitN, tiles_k, a.m, a.bits);
   if (a.cluster == 0 && a.workers <= 0) cluster = 0;
   int workers = cluster > 0 ? static_cast<int>(np / kUnitN) * cluster
                             : (a.workers > 0 ? a.workers : default_workers(a.m, a.k, a.n, a.bits));
@@ -411,9 +507,9 @@ void qgemm(const GemmArgs& a) {
       qgemm_tc(a, tiles_k, np / kUnitN, gp, props().sms, true, a.workspace, a.workspace_bytes);
     return;
   }
-  // M > 64 (peer outputs only): 64-row chunks, stream-ordered on one workspace.
-  for (int r0 = 0; r0 < a.m; r0 += 64) {
-    const int rows = std::min(64, a.m - r0);
+  // M > 32: 32-row chunks, stream-ordered on one workspace.
+  for (int r0 = 0; r0 < a.m; r0 += 32) {
+    const int rows = std::min(32, a.m - r0);
     const void* x = static_cast<const uint8_t*>(a.x) + static_cast<size_t>(r0) * a.k * 2;
     void* y = a.n_peers > 0
                   ? static_cast<void*>(static_cast<uint8_t*>(a.y_peers[0]) + static_cast<size_t>(r0) * a.ldy * 2)
@@ -480,7 +576,7 @@ __global__ void dequant_all_kernel(const uint32_t* __restrict__ vlut, const uint
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t a[4];
-      lut_dequant4(word_index_bytes<BITS>(lb, j), static_cast<uint32_t>(lane) * 4u, lut, sw, a);
+      lut_dequant4(atom_index_bytes<BITS>(lb, j), static_cast<uint32_t>(lane) * 4u, lut, sw, a);
 #pragma unroll
       for (int pp = 0; pp < 4; ++pp) {
         const int q = 4 * j + pp;

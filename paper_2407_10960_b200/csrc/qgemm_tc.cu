@@ -242,30 +242,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     fill_lut<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
     named_bar_sync(1, kDqWarps * 32);
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
-    // Device layout v2 (host_pack.cpp): a lane word = 4 consecutive k-steps
-    // (one "quad") of one 16-column atom.  KD = 128: warp w owns atom (w & 3),
-    // quad (w >> 2) of both units; KD = 64 (a stage holds quad (i & 1) of each
-    // unit): atom (w & 3) of unit w >> 2.
+    // KD = 128: warp w owns k-step w of both units; KD = 64: k-step (w & 3) of
+    // the stage's half of unit w >> 2 (local k-step kl within the stage)
     constexpr int kUnitsPerWarp = KD == 128 ? 2 : 1;
-    const int atom = warp & 3;
+    const int kl = KD == 128 ? warp : (warp & 3);
     const int u0 = KD == 128 ? 0 : (warp >> 2);
-    // this lane's word within a stage's unit bytes (KD = 64: quad-relative)
-    const int slot = (KD == 128 ? (warp >> 2) * 128 : 0) + atom * 32 + lane;
+    const int slot = kl * 32 + lane;  // this lane's slot within the stage's weight bytes
     const int g = lane >> 2, t = lane & 3;
-    // A-tile byte offset of this lane's pair p of k-step kstep, unit u (row n, k = kk, kk+1)
-    auto a_off = [&](int u, int kstep, int pp) -> uint32_t {
-      const int n = 64 * u + 16 * atom + g + 8 * (pp & 1);
-      const int kk = 16 * kstep + 2 * t + 8 * (pp >> 1);
+    // A-tile byte offset of this lane's pair p of atom j, unit u (row n, k = kk, kk+1)
+    auto a_off = [&](int u, int j, int pp) -> uint32_t {
+      const int n = 64 * u + 16 * j + g + 8 * (pp & 1);
+      const int kk = 16 * kl + 2 * t + 8 * (pp >> 1);
       const int at = kk >> 6, kin = kk & 63;
       return static_cast<uint32_t>(at * 16384 + (n >> 3) * 1024 + (n & 7) * 128 +
                                    ((((kin >> 3) ^ (n & 7))) << 4) + (kin & 7) * 2);
     };
-    const uint32_t s_lane = (lane >> 2) * 16 + atom * 4;
+    uint32_t aoff[kUnitsPerWarp][4][4];
+#pragma unroll
+    for (int uu = 0; uu < kUnitsPerWarp; ++uu)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) aoff[uu][j][pp] = a_off(u0 + uu, j, pp);
+    const uint32_t s_lane = (lane >> 2) * 16;
     for (int i = 0, s = 0, ph = 0; i < nk; ++i) {
       const int kt = kt_lo + i / (128 / KD);
-      const int quad = KD == 128 ? (warp >> 2) : (i & 1);
+      const int kstep = KD == 128 ? kl : kl + 4 * (i & 1);  // k-step within the unit
       mbar_wait(full_w(s), ph);
       const uint32_t st = stage(s);
+      const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt << 7) >> p.group_shift);
 #pragma unroll
       for (int uu = 0; uu < kUnitsPerWarp; ++uu) {
         const int u = u0 + uu;
@@ -280,16 +285,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           lb.hi = lds64(wr + slot * 8);
           lb.lo = lds32(wr + kStageW * 2 / 3 + slot * 4);  // 1-bit plane after the 2-bit plane
         }
-        const uint32_t sbase = st + kSOff + u * p.ng * 128 + s_lane;
+        const uint4 sq = lds128(st + kSOff + u * p.ng * 128 + gl * 128 + s_lane);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int kstep = 4 * quad + c;
-          const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt << 7) >> p.group_shift);
-          const uint32_t scw = lds32(sbase + gl * 128);
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t scw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
           uint32_t a[4];
-          lut_dequant4(word_index_bytes<BITS>(lb, c), lane4, lut, scw, a);
+          lut_dequant4(atom_index_bytes<BITS>(lb, j), lane4, lut, scw, a);
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) sts32(st + a_off(u, kstep, pp), a[pp]);
+          for (int pp = 0; pp < 4; ++pp) sts32(st + aoff[uu][j][pp], a[pp]);
         }
       }
       fence_proxy_async_smem();  // generic-proxy A stores -> visible to the tensor core
@@ -468,7 +471,7 @@ size_t tc_workspace_bytes(int m, int k, int n, int sms) {
   return splits > 1 ? static_cast<size_t>(splits) * m * n * 4 : 0;
 }
 
-bool tc_enabled(int m) { return m > 64 && std::getenv("FLUTE_NO_TC") == nullptr; }
+bool tc_enabled(int m) { return m >= 64 && std::getenv("FLUTE_NO_TC") == nullptr; }
 
 void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool zero_part,
               void* part, size_t part_bytes) {

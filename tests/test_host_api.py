@@ -93,20 +93,17 @@ def test_device_layout_bijective(F, bits, k, n, group):
 
 
 def test_device_layout_w4_register_order(F):
-    """Device layout v2: byte p of component c of lane slot
-    (quad*4 + j)*32 + lane holds pair (n = 16j+g+8(p&1), k = 16(4 quad + c) +
-    2t + 8(p>>1)), first weight in the high nibble."""
+    """Byte p of lane word j holds pair (n=16j+g+8(p&1), k=2t+8(p>>1)), first in
+    the high nibble."""
     k, n = 128, 64
-    for kstep in (0, 5):
-        idx = np.zeros((k, n), np.uint8)
-        idx[16 * kstep + 10, 21] = 0xA   # k%16=10 -> t=1, p>>1=1 ; n=21 -> j=1, g=5, p&1=0
-        idx[16 * kstep + 11, 21] = 0x3
-        dev = F.pack_device(idx, 4, 128)
-        lane = 5 * 4 + 1
-        quad, c = kstep >> 2, kstep & 3
-        slot = (quad * 4 + 1) * 32 + lane
-        assert dev[slot * 16 + c * 4 + 2] == 0xA3
-        assert np.count_nonzero(dev) == 1
+    idx = np.zeros((k, n), np.uint8)
+    idx[10, 21] = 0xA   # k=10 -> t=1, p>>1=1 ; n=21 -> j=1, g=5, p&1=0
+    idx[11, 21] = 0x3
+    dev = F.pack_device(idx, 4, 128)
+    lane = 5 * 4 + 1
+    # warp 0 (k in 0..15), lane, word j=1, byte p=2
+    assert dev[(0 * 32 + lane) * 16 + 1 * 4 + 2] == 0xA3
+    assert np.count_nonzero(dev) == 1
 
 
 def test_scales_device_layout(F):

@@ -286,114 +286,6 @@ __global__ void loop_tput(int iters, uint32_t* out) {
   if ((MODE == 0 || MODE == 3) && warp == 0) tmem_dealloc(t, 512);
 }
 
-
-// ---------------------------------------------------------------- D: UMMA rate
-// one thread issues `iters` TS UMMAs (M=64, N=NB, K=16) cycling over ND
-// accumulators; returns cycles per UMMA (issue to commit completion)
-template <int NB>
-__global__ void umma_rate(int iters, int nd, long long* out) {
-  extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint32_t slot;
-  __shared__ __align__(8) uint64_t bar;
-  const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 8192; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (warp == 0) tmem_alloc(smem_u32(&slot), 512);
-  if (threadIdx.x == 0) {
-    mbar_init(smem_u32(&bar), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t t = slot;
-  if (threadIdx.x == 0) {
-    const uint64_t bd = desc_sw128(smem_u32(sm));
-    const long long t0 = clock64();
-    for (int i = 0; i < iters; ++i) {
-      const int d = i % nd;
-      umma_ts(t + d * NB, t + 256 + 8 * (i & 7), bd, idesc_f16(64, NB), 1);
-    }
-    umma_commit(smem_u32(&bar));
-    mbar_wait(smem_u32(&bar), 0);
-    const long long t1 = clock64();
-    out[0] = t1 - t0;
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(t, 512);
-}
-
-// ---------------------------------------------------------------- E: st latency
-// each warp: iters x (tcgen05.st 16x128b.x8 [+ wait::st]); cycles per iteration
-__global__ void st_rate(int iters, int wait_each, long long* out) {
-  __shared__ uint32_t slot;
-  const int warp = threadIdx.x >> 5;
-  if (warp == 0) tmem_alloc(smem_u32(&slot), 512);
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t t = slot;
-  uint32_t v[16];
-  for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * 16 + i;
-  const uint32_t tw = t + (static_cast<uint32_t>((warp & 3) * 32 + ((warp >> 2) & 1) * 16) << 16);
-  const long long t0 = clock64();
-  for (int i = 0; i < iters; ++i) {
-    st_16x128_x8(tw + (i & 7) * 32, v);
-    if (wait_each) st_wait();
-    v[0] += 1;
-  }
-  st_wait();
-  const long long t1 = clock64();
-  if ((threadIdx.x & 31) == 0) out[warp] = t1 - t0;
-  fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(t, 512);
-}
-
-// SS / TS, M = 64 / 128, any N: cycles per UMMA (one issuing thread)
-__device__ __forceinline__ void umma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__global__ void umma_rate2(int iters, int M, int N, int ts, long long* out) {
-  extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint32_t slot;
-  __shared__ __align__(8) uint64_t bar;
-  const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 24576; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (warp == 0) tmem_alloc(smem_u32(&slot), 512);
-  if (threadIdx.x == 0) {
-    mbar_init(smem_u32(&bar), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t t = slot;
-  if (threadIdx.x == 0) {
-    const uint64_t bd = desc_sw128(smem_u32(sm) + 65536);
-    const uint64_t ad = desc_sw128(smem_u32(sm));
-    const uint32_t id = idesc_f16(M, N);
-    const long long t0 = clock64();
-    if (ts) {
-      for (int i = 0; i < iters; ++i) umma_ts(t, t + 256 + 8 * (i & 7), bd, id, 1);
-    } else {
-      for (int i = 0; i < iters; ++i) umma_ss(t, ad + 2 * (i & 3), bd, id, 1);
-    }
-    umma_commit(smem_u32(&bar));
-    mbar_wait(smem_u32(&bar), 0);
-    out[0] = clock64() - t0;
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(t, 512);
-}
-
 int main() {
   // ---- A
   uint32_t* d_out;
@@ -451,57 +343,6 @@ int main() {
   runB(std::integral_constant<int, 64>{}, std::integral_constant<int, 16>{});
   runB(std::integral_constant<int, 128>{}, std::integral_constant<int, 16>{});
   runB(std::integral_constant<int, 128>{}, std::integral_constant<int, 32>{});
-
-
-  {
-    long long* d_cyc;
-    CK(cudaMalloc(&d_cyc, 8));
-    CK(cudaFuncSetAttribute(umma_rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    for (int ts : {1, 0})
-      for (int M : {64, 128})
-        for (int N : {8, 16, 32, 64, 128, 256}) {
-          if (M == 128 && N < 16) continue;
-          if (ts && N > 224) continue;  // A lives at columns 256.. in this probe
-          umma_rate2<<<1, 128, 96 * 1024>>>(64, M, N, ts, d_cyc);
-          umma_rate2<<<1, 128, 96 * 1024>>>(2048, M, N, ts, d_cyc);
-          CK(cudaDeviceSynchronize());
-          long long c;
-          CK(cudaMemcpy(&c, d_cyc, 8, cudaMemcpyDeviceToHost));
-          const double cyc = c / 2048.0;
-          printf("UMMA %s M=%3d N=%3d K=16: %7.2f cycles/UMMA  %7.1f flop/clk\n", ts ? "TS" : "SS", M, N, cyc,
-                 2.0 * M * N * 16 / cyc);
-        }
-  }
-  // ---- D
-  {
-    long long* d_cyc;
-    CK(cudaMalloc(&d_cyc, 64 * 8));
-    auto rate = [&](auto kern, int nb) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      for (int nd : {1, 2, 4}) {
-        kern<<<1, 128, 40 * 1024>>>(64, nd, d_cyc);
-        kern<<<1, 128, 40 * 1024>>>(4096, nd, d_cyc);
-        CK(cudaDeviceSynchronize());
-        long long c;
-        CK(cudaMemcpy(&c, d_cyc, 8, cudaMemcpyDeviceToHost));
-        printf("UMMA TS M=64 N=%2d, %d accumulators: %6.2f cycles/UMMA\n", nb, nd, c / 4096.0);
-      }
-    };
-    rate(umma_rate<8>, 8);
-    rate(umma_rate<16>, 16);
-    rate(umma_rate<32>, 32);
-    rate(umma_rate<64>, 64);
-    for (int we : {1, 0}) {
-      for (int warps : {1, 4, 8}) {
-        st_rate<<<1, warps * 32>>>(4096, we, d_cyc);
-        CK(cudaDeviceSynchronize());
-        long long c[8];
-        CK(cudaMemcpy(c, d_cyc, warps * 8, cudaMemcpyDeviceToHost));
-        printf("tcgen05.st 16x128b.x8 %s, %d warps: %6.2f cycles/st per warp\n",
-               we ? "+ wait::st each" : "(one wait)", warps, c[0] / 4096.0);
-      }
-    }
-  }
   // ---- C
   const int iters = 4096;
   auto tput = [&](auto kern, const char* name) {
