@@ -497,8 +497,10 @@ class DeviceWeights:
         if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
             raise InputError(f"x must be a cuda float16 [m][{self.k}] tensor")
         x = x.contiguous()
-        if not 1 <= len(y_ptrs) <= 8 or any(int(p) == 0 for p in y_ptrs):
-            raise InputError("y_ptrs must hold 1..8 non-null device pointers")
+        if not 1 <= len(y_ptrs) <= 8:
+            raise ConfigError(f"y_ptrs must hold 1..8 device pointers, got {len(y_ptrs)}")
+        if any(int(p) == 0 for p in y_ptrs):
+            raise InputError("y_ptrs holds a null device pointer")
         if ycol0 < 0 or ldy < ycol0 + self.n:
             raise ConfigError(f"peer output needs ldy >= ycol0 + n ({ycol0} + {self.n})")
         arr = (C.c_void_p * len(y_ptrs))(*[int(p) for p in y_ptrs])
