@@ -213,6 +213,34 @@ int flute_qgemm_peers(const void* x, int m, int k, int n, const void* w, const v
 int flute_gemm_peers(flute_weights* w, const void* x_dev, int m, void* const* y_peers, int n_peers,
                      int ldy, int ycol0, int workers, void* stream);
 
+/* The N-sharded layer over the GPUs of one node, C++ host side
+ * (include/flutesim/sharded.hpp; no reference counterpart — the reference is
+ * one CPU process; each shard is its engine.cpp:345 GEMM on a column slice).
+ * NCCL is loaded at run time (libnccl.so.2 already in the process, else the
+ * system one).  Rank 0 calls flute_comm_unique_id and distributes the 128
+ * bytes out of band; every rank then calls flute_comm_create on its GPU. */
+#define FLUTE_COMM_ID_BYTES 128
+typedef struct flute_comm flute_comm;
+int flute_comm_unique_id(uint8_t* id_out /* FLUTE_COMM_ID_BYTES */);
+int flute_comm_create(const uint8_t* id, int world, int rank, flute_comm** out);
+int flute_comm_destroy(flute_comm* c);
+typedef struct flute_sharded flute_sharded;
+/* This rank's column shard of the FULL [k][n] matrix (host indices [k][n],
+ * scales [n][k/g], table values); max_m bounds flute_sharded_gemm_fused. */
+int flute_sharded_create(flute_comm* c, const uint8_t* indices, const uint16_t* scales,
+                         const float* table_values, int k, int n, int bits, int group, int max_m,
+                         flute_sharded** out);
+int flute_sharded_destroy(flute_sharded* s);
+int flute_sharded_info(const flute_sharded* s, int* n0, int* n1);
+/* y_dev [m][n] (full Y on every rank): shard GEMM + ncclAllGather + re-layout. */
+int flute_sharded_gemm(flute_sharded* s, const void* x_dev, int m, void* y_dev, void* stream);
+/* Fused: the GEMM epilogue stores this rank's columns into every rank's
+ * double-buffered output arena (CUDA IPC peer mappings), then a device
+ * release/acquire flag barrier; *y_out = this rank's full Y [m][n], valid
+ * until the call after next. */
+int flute_sharded_gemm_fused(flute_sharded* s, const void* x_dev, int m, const void** y_out,
+                             void* stream);
+
 /* The reference call itself: flutesim::execute (engine.hpp:72, engine.cpp:345)
  * on HOST buffers in the reference's canonical formats — x f16 [m][k],
  * canonical slices from reorder_and_split at `layout`, scales f16 [n][k/g],

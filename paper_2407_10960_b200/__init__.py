@@ -164,6 +164,15 @@ _SIGS = {
                                     _vp, C.c_size_t, C.c_int, _vp]),
     "flute_gemm_peers": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                    C.c_int, C.c_int, _vp]),
+    "flute_comm_unique_id": (C.c_int, [_u8p]),
+    "flute_comm_create": (C.c_int, [_u8p, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "flute_comm_destroy": (C.c_int, [_vp]),
+    "flute_sharded_create": (C.c_int, [_vp, _u8p, _u16p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.POINTER(_vp)]),
+    "flute_sharded_destroy": (C.c_int, [_vp]),
+    "flute_sharded_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "flute_sharded_gemm": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+    "flute_sharded_gemm_fused": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(_vp), _vp]),
     "flute_dequant_all_device": (C.c_int, [_u32p, C.c_int, _u16p, C.c_int, _u32p]),
     "flute_mma_fragment": (C.c_int, [_u16p, _u16p, _f32p, C.c_int, C.c_int, C.c_int]),
     "flute_debug_times": (C.c_int, [_u64p, C.c_int]),

@@ -14,6 +14,7 @@
 #include "flutesim/errors.hpp"
 #include "flutesim/mma.hpp"
 #include "flutesim/quantize.hpp"
+#include "flutesim/sharded.hpp"
 
 using namespace flutesim;
 
@@ -92,6 +93,13 @@ VectorizedTable table_from_words(const uint32_t* words, int bits) {
 }
 
 }  // namespace
+
+struct flute_comm {
+  std::unique_ptr<Communicator> impl;
+};
+struct flute_sharded {
+  std::unique_ptr<ShardedWeights> impl;
+};
 
 struct flute_weights {
   DeviceWeights* impl = nullptr;
@@ -758,6 +766,82 @@ int flute_gemm_peers(flute_weights* w, const void* x_dev, int m, void* const* y_
     need(w, "weights");
     w->impl->gemm_peers(static_cast<const Half*>(x_dev), m, y_peers, n_peers, ldy, ycol0, workers,
                         stream);
+  });
+}
+
+int flute_comm_unique_id(uint8_t* id_out) {
+  return guard([&] {
+    need(id_out, "id_out");
+    const std::vector<uint8_t> id = Communicator::unique_id();
+    std::memcpy(id_out, id.data(), id.size());
+  });
+}
+
+int flute_comm_create(const uint8_t* id, int world, int rank, flute_comm** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto c = std::make_unique<flute_comm>();
+    c->impl = std::make_unique<Communicator>(id, world, rank);
+    *out = c.release();
+  });
+}
+
+int flute_comm_destroy(flute_comm* c) {
+  return guard([&] { delete c; });
+}
+
+int flute_sharded_create(flute_comm* c, const uint8_t* indices, const uint16_t* scales,
+                         const float* table_values, int k, int n, int bits, int group, int max_m,
+                         flute_sharded** out) {
+  return guard([&] {
+    need(c, "comm");
+    need(indices, "indices");
+    need(scales, "scales");
+    need(table_values, "table_values");
+    need(out, "out");
+    *out = nullptr;
+    const QuantConfig cfg{bits, group};
+    cfg.validate(k);
+    if (n < 1) throw ConfigError("n must be >= 1");
+    std::vector<uint8_t> idx(indices, indices + static_cast<size_t>(k) * n);
+    const size_t ns = static_cast<size_t>(n) * (k / group);
+    std::vector<Half> sc(ns);
+    for (size_t i = 0; i < ns; ++i) sc[i] = Half::from_bits(scales[i]);
+    LookupTable t;
+    t.bits = bits;
+    t.values.assign(table_values, table_values + (size_t{1} << bits));
+    auto s = std::make_unique<flute_sharded>();
+    s->impl = std::make_unique<ShardedWeights>(*c->impl, idx, sc, t, k, n, cfg, max_m);
+    *out = s.release();
+  });
+}
+
+int flute_sharded_destroy(flute_sharded* s) {
+  return guard([&] { delete s; });
+}
+
+int flute_sharded_info(const flute_sharded* s, int* n0, int* n1) {
+  return guard([&] {
+    need(s, "sharded");
+    if (n0) *n0 = s->impl->n0();
+    if (n1) *n1 = s->impl->n1();
+  });
+}
+
+int flute_sharded_gemm(flute_sharded* s, const void* x_dev, int m, void* y_dev, void* stream) {
+  return guard([&] {
+    need(s, "sharded");
+    s->impl->gemm(static_cast<const Half*>(x_dev), m, static_cast<Half*>(y_dev), stream);
+  });
+}
+
+int flute_sharded_gemm_fused(flute_sharded* s, const void* x_dev, int m, const void** y_out,
+                             void* stream) {
+  return guard([&] {
+    need(s, "sharded");
+    need(y_out, "y_out");
+    *y_out = s->impl->gemm_fused(static_cast<const Half*>(x_dev), m, stream);
   });
 }
 

@@ -140,6 +140,14 @@ HostBatchGraph* host_batch_capture(const std::vector<HostBatchItem>& items);
 void host_batch_run(HostBatchGraph* g, void* stream);
 void host_batch_free(HostBatchGraph* g);
 
+// N-sharded layer (shard_kernels.cu): shard-major [P][m][w_max] all-gather
+// result -> row-major Y [m][n] (n0s_dev: P + 1 column starts, device); and the
+// release/acquire flag barrier of the fused path (flags[r]: rank r's [2][P]
+// flag array as mapped on this GPU).
+void shard_relayout(const void* gathered, void* y, int m, int n, int world, int w_max, const int* n0s_dev,
+                    void* stream);
+void peer_barrier(std::uint32_t* const* flags, int world, int me, int b, std::uint32_t epoch, void* stream);
+
 // Small RAII device buffer helpers used by the host layer.
 void* dev_alloc(std::size_t bytes);
 void dev_free(void* p);

@@ -232,8 +232,11 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
       mbar_init(full(s), 1);
       mbar_init(empty(s), 4);  // one arrive per warp of the stage's quartet
     }
-    mbar_init(epi_full, kConsumerWarps);
-    mbar_init(epi_empty, 1);
+    // every lane arrives on the partial-sum hand-off barriers (once per
+    // segment): each lane's own shared stores / loads are then ordered by its
+    // own release / the waiter's acquire
+    mbar_init(epi_full, kConsumerWarps * 32);
+    mbar_init(epi_empty, 32);
     if (p.cluster > 1) mbar_init(recv_bar, 32 * (p.cluster - 1));  // every sender lane arrives
     fence_mbar_init();
   }
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(epi_empty);
+      mbar_arrive(epi_empty);
 
       if (lane == 0) FLUTE_STAMP(tile == R.t_lo ? 5 : 4);
       const int t0 = tile * tiles_k;
@@ -670,7 +673,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
       for (int i = 0; i < C::kFrag; ++i)
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(row0 + i * rstride), "f"(accf[i]));
       __syncwarp();
-      if (lane == 0) mbar_arrive(epi_full);
+      mbar_arrive(epi_full);
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll

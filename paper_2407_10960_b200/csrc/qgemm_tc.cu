@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full_w(s), 1);
       mbar_init(full_x(s), 1);
       mbar_init(a_ready(s), kDqWarps);
-      mbar_init(empty(s), 1);
+      // the MMA commit (A / X read by the tensor core) + every dequant lane
+      // (its reads of the stage's weights and scales done)
+      mbar_init(empty(s), 1 + kDqWarps * 32);
     }
     mbar_init(acc_full, 1);
     fence_mbar_init();
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();  // generic-proxy A stores -> visible to the tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(a_ready(s));
+      mbar_arrive(empty(s));
       if (++s == S) {
         s = 0;
         ph ^= 1;

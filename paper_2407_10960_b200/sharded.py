@@ -129,6 +129,113 @@ class ShardedWeights:
             s.local.gemm_peers(x, ptrs, ldy=s.n, ycol0=s.range.n0, workers=workers)
 
 
+# ---------------------------------------------------------------------------
+# C++ host path (include/flutesim/sharded.hpp via the C ABI): NCCL loaded by the
+# library itself, fused path over CUDA IPC peer mappings + a device flag barrier
+# ---------------------------------------------------------------------------
+
+class NcclComm:
+    """flute_comm: one NCCL communicator owned by the C++ library.  The 128-byte
+    unique id is created on rank 0 and broadcast over an existing
+    torch.distributed group (any backend)."""
+
+    def __init__(self, rank: int, world: int, pg=None):
+        import ctypes as C
+        import torch.distributed as dist
+        from . import _check, _lib
+        self.rank, self.world = rank, world
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            _check(_lib.flute_comm_unique_id(uid))
+        if world > 1:
+            obj = [uid.tobytes()]
+            dist.broadcast_object_list(obj, src=0, group=pg)
+            uid = np.frombuffer(obj[0], np.uint8).copy()
+        h = C.c_void_p()
+        _check(_lib.flute_comm_create(uid, world, rank, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        from . import _lib
+        if getattr(self, "_h", None):
+            _lib.flute_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NativeShardedWeights:
+    """flute_sharded: this rank's column shard, C++ host side.  ``gemm`` =
+    shard GEMM + ncclAllGather + re-layout; ``gemm_fused`` = peer-store
+    epilogue into every rank's double-buffered arena + device flag barrier
+    (the returned tensor aliases the arena: valid until the call after next)."""
+
+    def __init__(self, comm: NcclComm, indices: np.ndarray, scales: np.ndarray,
+                 table_values: np.ndarray, bits: int, group: int, max_m: int = 32):
+        import ctypes as C
+        from . import _check, _lib
+        idx = np.ascontiguousarray(indices, np.uint8)
+        self.k, self.n = idx.shape
+        self.bits, self.group, self.max_m, self.comm = bits, group, max_m, comm
+        h = C.c_void_p()
+        _check(_lib.flute_sharded_create(comm._h, idx, np.ascontiguousarray(scales, np.uint16),
+                                         np.ascontiguousarray(table_values, np.float32), self.k,
+                                         self.n, bits, group, max_m, C.byref(h)))
+        self._h = h
+        n0, n1 = C.c_int(0), C.c_int(0)
+        _check(_lib.flute_sharded_info(h, C.byref(n0), C.byref(n1)))
+        self.n0, self.n1 = n0.value, n1.value
+
+    def gemm(self, x, y=None, stream=None):
+        import torch
+        from . import _check, _lib, _stream_ptr
+        x = x.contiguous()
+        if y is None:
+            y = torch.empty((x.shape[0], self.n), dtype=torch.float16, device=x.device)
+        _check(_lib.flute_sharded_gemm(self._h, x.data_ptr(), x.shape[0], y.data_ptr(),
+                                       _stream_ptr(stream)))
+        return y
+
+    def gemm_fused(self, x, stream=None):
+        """Full Y as a [m][n] view of the library's arena (no copy)."""
+        import ctypes as C
+        import torch
+        from . import _check, _lib, _stream_ptr
+        x = x.contiguous()
+        m = x.shape[0]
+        out = C.c_void_p()
+        _check(_lib.flute_sharded_gemm_fused(self._h, x.data_ptr(), m, C.byref(out),
+                                             _stream_ptr(stream)))
+        # wrap the arena pointer (lifetime = this object) without a copy
+        return _wrap_device_f16(out.value, (m, self.n), x.device)
+
+    def close(self):
+        from . import _lib
+        if getattr(self, "_h", None):
+            _lib.flute_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device_f16(ptr: int, shape, device):
+    """A torch view of an f16 device buffer owned by the library."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f2", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Arr(), device=device)
+
+
 def shard_from_device_layout(full_packed: np.ndarray, full_scales_dev: np.ndarray, r: ShardRange):
     """Cut a shard's device-layout weights / scales out of the full buffers
     (contiguous byte ranges; pure slicing, no re-pack)."""
@@ -155,5 +262,5 @@ def make_shards_single_process(indices, scales, table_values, bits, group, world
     return out
 
 
-__all__ = ["ShardedWeights", "gather_columns", "shard_columns", "shard_from_device_layout",
-           "make_shards_single_process"]
+__all__ = ["ShardedWeights", "NativeShardedWeights", "NcclComm", "gather_columns", "shard_columns",
+           "shard_from_device_layout", "make_shards_single_process"]

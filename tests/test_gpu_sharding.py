@@ -97,3 +97,32 @@ def test_sharded_weights_world1_nccl(F, orc, gpu):
         assert _within(y.cpu().numpy().view(np.uint16), y64)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m", [1, 5])
+def test_native_sharded_world1(F, gpu, m):
+    """The C++ sharded layer (flute_sharded_*: NCCL loaded by the library,
+    fused peer-store + device flag barrier) at world 1 on the one GPU: both
+    paths equal the plain device GEMM bitwise, repeatedly (the fused path's
+    double-buffered arena alternates and stays correct)."""
+    from paper_2407_10960_b200.sharded import NativeShardedWeights, NcclComm
+    rng = np.random.default_rng(77 + m)
+    k, n, bits, group = 1024, 512, 4, 128
+    idx, sc = F.quantize_matrix(rng.standard_normal((k, n)).astype(np.float32), bits, group)
+    table = F.build_nf_table(bits)
+    comm = NcclComm(0, 1)
+    sw = NativeShardedWeights(comm, idx, sc, table, bits, group, max_m=8)
+    assert (sw.n0, sw.n1) == (0, n)
+    dw = F.DeviceWeights(idx, sc, table, bits, group)
+    for it in range(4):
+        x = (gpu.randn(m, k, device="cuda") * 0.5).half()
+        want = dw.gemm(x).cpu()
+        got = sw.gemm(x).cpu()
+        fused = sw.gemm_fused(x).clone().cpu()
+        gpu.cuda.synchronize()
+        assert gpu.equal(got.view(gpu.int16), want.view(gpu.int16)), it
+        assert gpu.equal(fused.view(gpu.int16), want.view(gpu.int16)), it
+    with pytest.raises(F.ConfigError):
+        sw.gemm_fused((gpu.randn(9, k, device="cuda")).half())  # m > max_m
+    sw.close()
+    comm.close()

@@ -23,7 +23,13 @@ KEYS = [
     ("launch__occupancy_limit_shared_mem", "occ_lim_smem"),
     ("launch__occupancy_limit_registers", "occ_lim_regs"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_%"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_%"),
+    ("lts__t_bytes.sum", "l2_bytes"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%"),
 ]
+# tensor-pipe counters (names differ across architectures: every raw metric
+# mentioning the tensor / tcgen05 pipes is printed)
+TENSOR_HINTS = ("pipe_tensor", "pipe_tc", "tcgen05", "umma", "tmem")
 
 
 def rows(rep):
@@ -43,6 +49,9 @@ def main():
                 if k in h:
                     i = h.index(k)
                     print(f"  {lab:18s} {row[i]:>14s} {units[i]}")
+            for i, k in enumerate(h):
+                if any(t in k for t in TENSOR_HINTS) and (k.endswith(".sum") or "pct" in k):
+                    print(f"  {k[:60]:60s} {row[i]:>14s} {units[i]}")
             st = []
             for i, k in enumerate(h):
                 if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):

@@ -1,0 +1,64 @@
+#!/usr/bin/env python
+"""Small launches of every device protocol, for compute-sanitizer
+(memcheck / racecheck / synccheck):
+  * Stream-K with data-polling fixup (explicit workers, no cluster),
+  * Stream-K with ticketed worker ids (workers > co-resident slots),
+  * cluster split-K through DSMEM (FLUTE_FORCE_CLUSTER),
+  * the tcgen05/TMEM kernel (M >= 64) with split-K partials,
+  * the default decompositions of the M <= 32 kernel (cluster split-K /
+    whole tiles) at a larger K,
+each checked against binary64 so a sanitizer run also proves the results.
+usage: compute-sanitizer --tool racecheck python tools/sanitize_cases.py [case ...]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2407_10960_b200 as F  # noqa: E402
+from oracle import Oracle  # noqa: E402  (checker only)
+
+orc = Oracle()
+
+
+def run(name, m, k, n, bits, group, workers=0, env=None):
+    for kk, v in (env or {}).items():
+        os.environ[kk] = v
+    rng = np.random.default_rng(m + k + n + bits)
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    idx, sc = F.quantize_matrix(w, bits, group)
+    table = F.build_nf_table(bits)
+    x16 = (rng.standard_normal((m, k)) * 0.5).astype(np.float16)
+    dw = F.DeviceWeights(idx, sc, table, bits, group)
+    x = torch.from_numpy(x16).cuda()
+    for _ in range(2):  # twice: the second launch reuses the re-armed workspace
+        y = dw.gemm(x, workers=workers)
+    torch.cuda.synchronize()
+    y = y.cpu().numpy().astype(np.float64)
+    y64 = orc.reference_f64(x16.view(np.uint16), idx, bits, group, sc, table)
+    bound = 1e-2 * np.maximum(np.abs(y64), np.sqrt(np.mean(y64 ** 2)))
+    ok = bool(np.all(np.abs(y - y64) <= bound))
+    print(f"{name:28s} m={m} k={k} n={n} W{bits}g{group} workers={workers or 'default'}: "
+          f"{'ok' if ok else 'MISMATCH'}", flush=True)
+    for kk in (env or {}):
+        del os.environ[kk]
+    return ok
+
+
+CASES = {
+    "streamk": lambda: run("streamk fixup", 3, 1024, 256, 4, 128, workers=7),
+    "streamk_w3": lambda: run("streamk fixup W3", 9, 1024, 192, 3, 64, workers=5),
+    "ticket": lambda: run("streamk ticketed", 1, 2048, 512, 3, 128, workers=400),
+    "cluster": lambda: run("cluster split-K", 2, 1024, 256, 4, 128, env={"FLUTE_FORCE_CLUSTER": "4"}),
+    "tcgen05": lambda: run("tcgen05 split-K", 128, 1024, 256, 4, 128, env={"FLUTE_TC_SPLITS": "2"}),
+    "tcgen05_bn256": lambda: run("tcgen05 BN=256", 256, 512, 256, 3, 128, env={"FLUTE_TC_BN": "256"}),
+    "default": lambda: run("default decomposition", 1, 4096, 512, 4, 128),
+    "default_m32": lambda: run("default decomposition M=32", 32, 2048, 384, 3, 128),
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    ok = all([CASES[n]() for n in names])
+    sys.exit(0 if ok else 1)

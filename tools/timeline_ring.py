@@ -26,17 +26,18 @@ def main():
     dws = [F.DeviceWeights(idx, sc, F.build_nf_table(bits), bits, group) for _ in range(L)]
     x = torch.randn(m, k, dtype=torch.float16, device="cuda")
     y = torch.empty(m, n, dtype=torch.float16, device="cuda")
-    P = F.default_workers(m, k, n, bits)
+    W = int(os.environ.get("WORKERS", "0"))
+    P = W or F.default_workers(m, k, n, bits)
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
         for i in range(L):  # warm (fills the ring once)
-            dws[i].gemm(x, y, stream=st.cuda_stream)
+            dws[i].gemm(x, y, workers=W, stream=st.cuda_stream)
     st.synchronize()
     if os.environ.get("GRAPH"):  # same launches captured into a CUDA graph and replayed
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
             for i in range(L):
-                dws[i].gemm(x, y, stream=st.cuda_stream)
+                dws[i].gemm(x, y, workers=W, stream=st.cuda_stream)
         g.replay()
         st.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -49,7 +50,7 @@ def main():
     else:
         with torch.cuda.stream(st):
             for i in range(L):
-                dws[i].gemm(x, y, stream=st.cuda_stream)
+                dws[i].gemm(x, y, workers=W, stream=st.cuda_stream)
     st.synchronize()
     res = F.debug_times(P, L)
     t0 = min(int(r[0][:, 0][r[0][:, 0] > 0].min()) for r in res)
