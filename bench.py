@@ -464,10 +464,14 @@ def run_ours(args):
                          # ncu dram__bytes_read.sum + dram__bytes_write.sum of one
                          # W3 M=1 4096x14336 launch (profiles/); its algorithmic
                          # bytes are 22,974,480 (no re-reads)
-                         "traffic": 23003136,
-                         "traffic_case": "W3 g128 M=1 K=4096 N=14336, DRAM bytes per launch (ncu)",
-                         "kernel": "qgemm_mma_kernel<BITS,BM,...> = every launch of the step "
-                                   "(achieved = step bytes / step time)"},
+                         "traffic": 23003136 if args.workload == "headline" else None,
+                         "traffic_case": ("W3 g128 M=1 K=4096 N=14336, DRAM bytes per launch (ncu)"
+                                          if args.workload == "headline" else None),
+                         "kernel": ("qgemm_tc_kernel<4,BN> (+ splitk_reduce_kernel) = every launch "
+                                    "of the step (achieved = step FLOPs / step time)"
+                                    if args.workload == "tc" else
+                                    "qgemm_mma_kernel<BITS,BM,...> = every launch of the step "
+                                    "(achieved = step bytes / step time)")},
             "e2e": e2e,
             "gpu_launches": steps * len(cases),
             "clocks": clocks,
@@ -560,7 +564,7 @@ def run_sharded_70b(args):
     import torch
     import torch.distributed as dist
     import paper_2407_10960_b200 as F
-    from paper_2407_10960_b200.sharded import ShardedWeights
+    from paper_2407_10960_b200.sharded import NativeShardedWeights, NcclComm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -577,12 +581,22 @@ def run_sharded_70b(args):
     table = F.build_nf_table(bits)
     shard_bytes = F.shard_range(k, n, bits, group, world, rank).w_bytes
     reps = max(2, int(np.ceil(3 * 126e6 / shard_bytes)))
-    sws = [ShardedWeights(idx, scales, table, bits, group, rank, world, mode=args.allgather)
+    comm = NcclComm(rank, world)  # C++ communicator (NCCL loaded by the library)
+    sws = [NativeShardedWeights(comm, idx, scales, table, bits, group, max_m=m)
            for _ in range(min(reps, 24))]
     x = torch.from_numpy((rng.standard_normal((m, k)) * 0.5).astype(np.float16)).cuda()
+    y = torch.empty((m, n), dtype=torch.float16, device="cuda")
     layer_bytes = algo_bytes(m, k, n, bits, group)
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step(i):
+        if args.allgather == "peer":
+            sws[i % len(sws)].gemm_fused(x, stream=stream)
+        else:
+            sws[i % len(sws)].gemm(x, y, stream=stream)
+
     for i in range(warmup):
-        sws[i % len(sws)].gemm(x)
+        step(i)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -592,7 +606,7 @@ def run_sharded_70b(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(steps):
-        sws[i % len(sws)].gemm(x)
+        step(i)
     e1.record()
     e1.synchronize()
     torch.cuda.synchronize()
@@ -612,13 +626,19 @@ def run_sharded_70b(args):
             "vs_baseline": None, "dtype": "f16", "data": "synthetic (N(0,1) weights NF4 g128)",
             "config": {"workload": "BASELINE configs[3]: LLaMA-3-70B layer K=8192 N=28672 W4 g128 "
                                    "M=1, N-sharded + output all-gather",
-                       "allgather": args.allgather, "layer_bytes": layer_bytes,
+                       "allgather": args.allgather + (" (flute_sharded_gemm: shard GEMM + ncclAllGather)"
+                                                      if args.allgather == "nccl" else
+                                                      " (flute_sharded_gemm_fused: peer-store epilogue + "
+                                                      "device flag barrier)"),
+                       "layer_bytes": layer_bytes,
                        "l2": f"{len(sws)} weight replicas rotated (>= 3x L2 per rank)"},
             "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(per_gpu / peak, 4), "peak_kind": peak_kind,
                          "note": "per-GPU shard bytes / step time (includes the all-gather)"},
             "gpu_launches": steps, "clocks": clocks}), flush=True)
     dist.barrier()
+    del sws
+    comm.close()
     dist.destroy_process_group()
     return 0
 

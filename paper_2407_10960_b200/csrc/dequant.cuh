@@ -81,6 +81,39 @@ __device__ __forceinline__ void lut_dequant4(uint32_t idx_bytes, uint32_t lane4,
   }
 }
 
+// Compact-table variant (128-byte rows: the 32 lane copies only, no partial-
+// sum rows in the gaps): one PRMT puts idx << 8 | lane*8 together and a shift
+// halves it to idx * 128 + lane * 4.
+__device__ __forceinline__ void lut_dequant4_r128(uint32_t idx_bytes, uint32_t lane8, uint32_t lut_base,
+                                                  uint32_t scales, uint32_t (&a)[4]) {
+  const __half2 s2 = *reinterpret_cast<const __half2*>(&scales);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t off = prmt(idx_bytes, lane8, 0x5504u | (static_cast<uint32_t>(p) << 4)) >> 1;
+    uint32_t v = lds32_const(lut_base + off);
+    const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&v),
+                              (p & 1) ? __high2half2(s2) : __low2half2(s2));
+    a[p] = *reinterpret_cast<const uint32_t*>(&r);
+  }
+}
+template <int BITS, int NTHREADS>
+__device__ __forceinline__ void fill_lut_r128(uint32_t lut_base, const uint32_t* __restrict__ vlut, int tid) {
+  constexpr int kEntries = 1 << (2 * BITS);
+  constexpr int kChunks = kEntries * 8;  // 8 x 16-byte chunks = the 32 lane copies
+  constexpr int kPer = (kChunks + NTHREADS - 1) / NTHREADS;
+  uint32_t v[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int c = tid + i * NTHREADS;
+    v[i] = c < kChunks ? __ldg(vlut + (c >> 3)) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int c = tid + i * NTHREADS;
+    if (c < kChunks) sts128(lut_base + (c >> 3) * 128 + (c & 7) * 16, make_uint4(v[i], v[i], v[i], v[i]));
+  }
+}
+
 // The two halves of lut_dequant4, for callers that batch the lookups of
 // several atoms ahead of their MMAs (more loads in flight per warp).
 __device__ __forceinline__ void lut_lookup4(uint32_t idx_bytes, uint32_t lane4, uint32_t lut_base,

@@ -26,7 +26,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <string>
 #include <type_traits>
 
@@ -39,12 +41,20 @@ namespace flute_dev {
 
 namespace tc {
 
-constexpr int kDqWarps = 8;
-constexpr int kTmaWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kThreads = 320;
+// 16 dequant warps in two groups of 8 taking 64-k stages alternately (the
+// per-stage dequant is latency-bound: two stages in flight per SM), then
+// the producers and the MMA issuer.
+constexpr int kDqWarps = 16;
+constexpr int kGroupWarps = 8;
+constexpr int kWWarp = 16;  // weights + scales producer
+constexpr int kMmaWarp = 17;
+constexpr int kXWarp = 18;  // X producer
+constexpr int kThreads = 32 * 19;
 constexpr int kUnitK = 128;
-constexpr int kMaxStages = 4;
+constexpr int kMaxW = 8, kMaxA = 4, kMaxX = 4;
+// A W-ring slot holds kWK whole units (128 k each) of both n-tiles: one bulk
+// copy of weights and one of scales per n-tile and slot (few, large copies).
+constexpr int kWK = 2;
 
 struct Params {
   const uint8_t* w;
@@ -58,10 +68,36 @@ struct Params {
   int gp;        // padded groups per column
   int group_shift;
   int splits;
-  int stages;
-  int ng;  // scale groups per unit in a stage's scale block (>= 1)
-  uint32_t lut_bytes, bar_off, stage_off, stage_bytes;
+  int sw, sx, sa;  // W / X / A ring depths
+  int ngw;       // scale groups of one n-tile in a W slot (kWK units, + 1 for an unaligned start)
+  uint32_t bar_off, a_off, x_off, w_off, w_stage;
+  unsigned long long* trace;  // diag build, FLUTE_TC_TRACE: [cta][4] + [cta][64 stages][4] (ns)
 };
+
+__device__ __forceinline__ unsigned long long tc_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef FLUTE_DIAGNOSTICS
+#define TC_TRACE(slot, v)                                                                     \
+  do {                                                                                        \
+    if (p.trace) p.trace[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 4 + (slot)] = (v); \
+  } while (0)
+#define TC_STAGE(i, slot)                                                                      \
+  do {                                                                                         \
+    if (p.trace && (i) < 64)                                                                   \
+      p.trace[static_cast<size_t>(gridDim.x * gridDim.y * gridDim.z) * 4 +                     \
+              ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 64 + (i)) * 4 + (slot)] = tc_now(); \
+  } while (0)
+#else
+#define TC_TRACE(slot, v) \
+  do {                    \
+  } while (0)
+#define TC_STAGE(i, slot) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
   // K-major, 128B swizzle: start >> 4, LBO = 1 (unused for swizzled K-major),
@@ -90,53 +126,52 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
-// KD = stage depth: 128 (one unit per stage, two 64-k swizzle atoms) or 64
-// (half a unit: one atom, so a BN = 256 X tile still double-buffers within
-// shared memory; the 8 dequant warps then split as 2 units x 4 k-steps).
-template <int BITS, int BN, int KD>
+// Ring position of item i in a ring of `depth` slots.
+struct Slot {
+  int s;
+  uint32_t ph;
+  __device__ __forceinline__ Slot(int i, int depth) : s(i % depth), ph(static_cast<uint32_t>(i / depth) & 1u) {}
+};
+
+// Stages are 64 k deep (one 128B-swizzle atom of the A and X tiles): stage i
+// covers k [kt*128 + 64*h, +64) with kt = kt_lo + i/2, h = i & 1.  Three
+// independent rings so each resource runs as far ahead as its size allows:
+//  * W ring (sw slots): the two units' packed weights for the stage + their
+//    group scales, filled by the W warp (the first sw stages before the
+//    programmatic-dependent-launch wait — weights do not depend on the
+//    previous kernel); freed by every dequant lane once read;
+//  * A ring (2 slots): the dequantised W^T tile [128 n][64 k] f16, K-major
+//    SW128, written by the 8 dequant warps; freed by the MMA commit;
+//  * X ring (sx slots): the X tile [BN rows][64 k] (one TMA box, the
+//    canonical K-major SW128 UMMA layout), filled by the X warp after the
+//    PDL wait; freed by the MMA commit.
+template <int BITS, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  static_assert(KD == 128 || KD == 64, "stage depth");
-  constexpr int kAtoms = KD / 64;             // 64-k swizzle atoms per stage
-  constexpr int kSubBytes = BITS * 1024;      // one unit's packed weights
-  constexpr int kStageW = kSubBytes * KD / 128;  // per unit per stage
-  constexpr uint32_t kABytes = kAtoms * 16384;   // kAtoms 64-k swizzle atoms of 128 rows
-  constexpr uint32_t kXBox = BN * 128;      // one 64-k box of BN rows
-  constexpr uint32_t kWOff = kABytes + kAtoms * kXBox;
-  constexpr uint32_t kSOff = kWOff + 2 * kStageW;
+  constexpr int kSubBytes = BITS * 1024;      // one unit's packed weights (128 k)
+  constexpr int kSlotW = kWK * kSubBytes;      // one n-tile's weights in a W slot
+  constexpr uint32_t kABytes = 16384;          // [128 n][64 k] f16
+  constexpr uint32_t kXBytes = BN * 128;       // [BN rows][64 k] f16
 
   const uint32_t base = smem_u32(smem);
   const uint32_t lut = base;
   const uint32_t bars = base + p.bar_off;
-  const int S = p.stages;
-  auto full_w = [&](int s) { return bars + 8 * s; };
-  auto full_x = [&](int s) { return bars + 8 * (kMaxStages + s); };
-  auto a_ready = [&](int s) { return bars + 8 * (2 * kMaxStages + s); };
-  auto empty = [&](int s) { return bars + 8 * (3 * kMaxStages + s); };
-  const uint32_t acc_full = bars + 8 * (4 * kMaxStages);
+  auto w_full = [&](int s) { return bars + 8 * s; };
+  auto w_empty = [&](int s) { return bars + 8 * (kMaxW + s); };
+  auto a_full = [&](int s) { return bars + 8 * (2 * kMaxW + s); };
+  auto a_empty = [&](int s) { return bars + 8 * (2 * kMaxW + kMaxA + s); };
+  auto x_full = [&](int s) { return bars + 8 * (2 * kMaxW + 2 * kMaxA + s); };
+  auto x_empty = [&](int s) { return bars + 8 * (2 * kMaxW + 2 * kMaxA + kMaxX + s); };
+  const uint32_t acc_full = bars + 8 * (2 * kMaxW + 2 * kMaxA + 2 * kMaxX);
   const uint32_t tmem_slot = acc_full + 8;  // tcgen05.alloc writes the TMEM base here
-  auto stage = [&](int s) { return base + p.stage_off + s * p.stage_bytes; };
+  auto a_at = [&](int s) { return base + p.a_off + s * kABytes; };
+  auto x_at = [&](int s) { return base + p.x_off + s * kXBytes; };
+  auto w_at = [&](int s) { return base + p.w_off + s * p.w_stage; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x;  // 128-column tile = units' n-tiles 2*pair, 2*pair+1
@@ -144,18 +179,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int z = blockIdx.z;
   const int kt_lo = z * p.tiles_k / p.splits;
   const int kt_hi = (z + 1) * p.tiles_k / p.splits;
-  const int nk = (kt_hi - kt_lo) * (128 / KD);  // stages
+  const int nk = (kt_hi - kt_lo) * 2;  // 64-deep stages
   const int nt0 = 2 * pair;
   const bool has_u1 = nt0 + 1 < p.tiles_n;
+  const int SW = p.sw, SX = p.sx, SA = p.sa;
+  if (threadIdx.x == 0) TC_TRACE(0, tc_now());
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full_w(s), 1);
-      mbar_init(full_x(s), 1);
-      mbar_init(a_ready(s), kDqWarps);
-      // the MMA commit (A / X read by the tensor core) + every dequant lane
-      // (its reads of the stage's weights and scales done)
-      mbar_init(empty(s), 1 + kDqWarps * 32);
+    for (int s = 0; s < SW; ++s) {
+      mbar_init(w_full(s), 1);
+      mbar_init(w_empty(s), kDqWarps * 32);
+    }
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(a_full(s), kGroupWarps * 32);  // the stage's group
+      mbar_init(a_empty(s), 1);
+    }
+    for (int s = 0; s < SX; ++s) {
+      mbar_init(x_full(s), 1);
+      mbar_init(x_empty(s), 1);
     }
     mbar_init(acc_full, 1);
     fence_mbar_init();
@@ -167,175 +208,224 @@ __global__ void __launch_bounds__(kThreads, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  tc_fence_before();
+  tmem_fence_before();
   __syncthreads();
-  tc_fence_after();
+  tmem_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + (tmem_slot - base));
   pdl_launch_dependents();
 
-  if (warp == kTmaWarp) {
-    // ===================== TMA producer =====================
+  if (warp == kWWarp) {
+    // ===================== weights + scales producer =====================
     if (elect_one()) {
-      prefetch_tmap(&tmap_x);
       const uint64_t pol = policy_evict_first();
       const int units_pair = has_u1 ? 2 : 1;
-      for (int i = 0, s = 0, ph = 0; i < nk; ++i) {
-        const int kt = kt_lo + i / (128 / KD);
-        const int half = KD == 64 ? (i & 1) : 0;  // which 64-k half of the unit
-        if (i >= S) mbar_wait(empty(s), ph ^ 1);
-        const uint32_t st = stage(s);
-        const int glo = (kt * kUnitK) >> p.group_shift;
-        const uint32_t sb = p.ng * 128;
-        mbar_arrive_expect_tx(full_w(s), units_pair * (kStageW + sb));
+      const int nw = (kt_hi - kt_lo + kWK - 1) / kWK;  // W slots
+      for (int j = 0; j < nw; ++j) {
+        const Slot ws(j, SW);
+        if (j >= SW) mbar_wait(w_empty(ws.s), ws.ph ^ 1u);
+        const int kt0 = kt_lo + j * kWK;
+        const int nu = kt_hi - kt0 < kWK ? kt_hi - kt0 : kWK;
+        const int glo = (kt0 * kUnitK) >> p.group_shift;
+        const int ng = ((((kt0 + nu) * kUnitK) - 1) >> p.group_shift) - glo + 1;
+        const uint32_t st = w_at(ws.s);
+        mbar_arrive_expect_tx(w_full(ws.s), units_pair * (nu * kSubBytes + ng * 128));
         for (int u = 0; u < units_pair; ++u) {
-          const size_t unit = static_cast<size_t>(nt0 + u) * p.tiles_k + kt;
-          const uint8_t* wu = p.w + unit * kSubBytes;
-          if constexpr (KD == 128) {
-            bulk_g2s_hint(st + kWOff + u * kStageW, wu, kSubBytes, full_w(s), pol);
-          } else if constexpr (BITS == 3) {
-            // k-steps 4h..4h+3: 2-bit plane bytes [1024h, +1024), 1-bit [2048 + 512h, +512)
-            bulk_g2s_hint(st + kWOff + u * kStageW, wu + 1024 * half, 1024, full_w(s), pol);
-            bulk_g2s_hint(st + kWOff + u * kStageW + 1024, wu + 2048 + 512 * half, 512, full_w(s), pol);
-          } else {
-            bulk_g2s_hint(st + kWOff + u * kStageW, wu + kStageW * half, kStageW, full_w(s), pol);
-          }
-          bulk_g2s(st + kSOff + u * sb, p.sc + (static_cast<size_t>(nt0 + u) * p.gp + glo) * 128, sb,
-                   full_w(s));
+          const size_t unit = static_cast<size_t>(nt0 + u) * p.tiles_k + kt0;
+          bulk_g2s_hint(st + u * kSlotW, p.w + unit * kSubBytes, nu * kSubBytes, w_full(ws.s), pol);
+          bulk_g2s(st + 2 * kSlotW + u * p.ngw * 128, p.sc + (static_cast<size_t>(nt0 + u) * p.gp + glo) * 128,
+                   ng * 128, w_full(ws.s));
         }
-        if (i == 0) pdl_wait();  // X belongs to the previous kernel in the stream
-        mbar_arrive_expect_tx(full_x(s), kAtoms * kXBox);
-#pragma unroll
-        for (int a = 0; a < kAtoms; ++a)
-          tma_2d_g2s(st + kABytes + a * kXBox, &tmap_x, kt * kUnitK + 64 * (half + a), m0, full_x(s));
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
-        }
+      }
+    }
+  } else if (warp == kXWarp) {
+    // ===================== X producer =====================
+    if (elect_one()) {
+      prefetch_tmap(&tmap_x);
+      pdl_wait();  // X belongs to the previous kernel in the stream
+      for (int i = 0; i < nk; ++i) {
+        const Slot xs(i, SX);
+        if (i >= SX) mbar_wait(x_empty(xs.s), xs.ph ^ 1u);
+        const int kt = kt_lo + (i >> 1), h = i & 1;
+        mbar_arrive_expect_tx(x_full(xs.s), kXBytes);
+        tma_2d_g2s(x_at(xs.s), &tmap_x, kt * kUnitK + 64 * h, m0, x_full(xs.s));
       }
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer =====================
     constexpr uint32_t idesc = instr_desc<BN>();
-    for (int i = 0, s = 0, ph = 0; i < nk; ++i) {
-      mbar_wait(full_x(s), ph);
-      mbar_wait(a_ready(s), ph);
-      tc_fence_after();
-      const uint32_t st = stage(s);
+    for (int i = 0; i < nk; ++i) {
+      const Slot as(i, SA), xs(i, SX);
+      mbar_wait(a_full(as.s), as.ph);
+      mbar_wait(x_full(xs.s), xs.ph);
+      if (lane == 0) TC_STAGE(i, 3);
+      tmem_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int a = 0; a < kAtoms; ++a)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = smem_desc_sw128(st + a * 16384 + kk * 32);
-            const uint64_t bd = smem_desc_sw128(st + kABytes + a * kXBox + kk * 32);
-            umma_f16(tmem, ad, bd, idesc, (i | a | kk) != 0 ? 1u : 0u);
-          }
-        umma_commit(empty(s));  // smem stage free once these MMAs have read it
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = smem_desc_sw128(a_at(as.s) + kk * 32);
+          const uint64_t bd = smem_desc_sw128(x_at(xs.s) + kk * 32);
+          umma_f16(tmem, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(a_empty(as.s));  // A / X slots free once these MMAs have read them
+        umma_commit(x_empty(xs.s));
         if (i == nk - 1) umma_commit(acc_full);
       }
       __syncwarp();
-      if (++s == S) {
-        s = 0;
-        ph ^= 1;
-      }
     }
   } else {
-    // ===================== dequant warps (0..7) =====================
-    fill_lut<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
+    // ===================== dequant warps (0..15) =====================
+    fill_lut_r128<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
     named_bar_sync(1, kDqWarps * 32);
-    const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
-    // KD = 128: warp w owns k-step w of both units; KD = 64: k-step (w & 3) of
-    // the stage's half of unit w >> 2 (local k-step kl within the stage)
-    constexpr int kUnitsPerWarp = KD == 128 ? 2 : 1;
-    const int kl = KD == 128 ? warp : (warp & 3);
-    const int u0 = KD == 128 ? 0 : (warp >> 2);
-    const int slot = kl * 32 + lane;  // this lane's slot within the stage's weight bytes
+    const uint32_t lane8 = static_cast<uint32_t>(lane) * 8u;
+    // group grp = warp >> 3 takes stages i with i % 2 == grp; its warp wl:
+    // local k-step kl = wl & 3 of the stage's 64 k, unit u = wl >> 2
+    const int grp = warp >> 3;
+    const int wl = warp & 7;
+    const int kl = wl & 3;
+    const int u = wl >> 2;
     const int g = lane >> 2, t = lane & 3;
-    // A-tile byte offset of this lane's pair p of atom j, unit u (row n, k = kk, kk+1)
-    auto a_off = [&](int u, int j, int pp) -> uint32_t {
-      const int n = 64 * u + 16 * j + g + 8 * (pp & 1);
-      const int kk = 16 * kl + 2 * t + 8 * (pp >> 1);
-      const int at = kk >> 6, kin = kk & 63;
-      return static_cast<uint32_t>(at * 16384 + (n >> 3) * 1024 + (n & 7) * 128 +
-                                   ((((kin >> 3) ^ (n & 7))) << 4) + (kin & 7) * 2);
-    };
-    uint32_t aoff[kUnitsPerWarp][4][4];
+    // A-tile byte offset of this lane's pair p of atom j (row n, k = kk, kk+1)
+    uint32_t aoff[4][4];
 #pragma unroll
-    for (int uu = 0; uu < kUnitsPerWarp; ++uu)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int pp = 0; pp < 4; ++pp) aoff[uu][j][pp] = a_off(u0 + uu, j, pp);
+      for (int pp = 0; pp < 4; ++pp) {
+        const int n = 64 * u + 16 * j + g + 8 * (pp & 1);
+        const int kk = 16 * kl + 2 * t + 8 * (pp >> 1);
+        aoff[j][pp] = static_cast<uint32_t>((n >> 3) * 1024 + (n & 7) * 128 + (((kk >> 3) ^ (n & 7)) << 4) +
+                                            (kk & 7) * 2);
+      }
     const uint32_t s_lane = (lane >> 2) * 16;
-    for (int i = 0, s = 0, ph = 0; i < nk; ++i) {
-      const int kt = kt_lo + i / (128 / KD);
-      const int kstep = KD == 128 ? kl : kl + 4 * (i & 1);  // k-step within the unit
-      mbar_wait(full_w(s), ph);
-      const uint32_t st = stage(s);
-      const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt << 7) >> p.group_shift);
-#pragma unroll
-      for (int uu = 0; uu < kUnitsPerWarp; ++uu) {
-        const int u = u0 + uu;
-        if (u == 1 && !has_u1) break;
-        const uint32_t wr = st + kWOff + u * kStageW;
-        LaneBits<BITS> lb;
+    const bool active = u == 0 || has_u1;
+    for (int i = grp; i < nk; i += 2) {
+      const int j = i / (2 * kWK);         // W slot sequence number
+      const int r = (i >> 1) % kWK;        // unit within the slot
+      const Slot ws(j, SW), as(i, SA);
+      const int kt = kt_lo + (i >> 1), h = i & 1;
+      const int kstep = kl + 4 * h;  // k-step within the unit
+      const int slot_u = kstep * 32 + lane;
+      mbar_wait(w_full(ws.s), ws.ph);
+      if ((threadIdx.x & 255) == 0) TC_STAGE(i, 0);
+      const uint32_t st = w_at(ws.s);
+      LaneBits<BITS> lb;
+      uint4 sq = make_uint4(0u, 0u, 0u, 0u);
+      if (active) {
+        const uint32_t wr = st + u * kSlotW + r * kSubBytes;
         if constexpr (BITS == 4) {
-          lb.w = lds128(wr + slot * 16);
+          lb.w = lds128(wr + slot_u * 16);
         } else if constexpr (BITS == 2) {
-          lb.w = lds64(wr + slot * 8);
+          lb.w = lds64(wr + slot_u * 8);
         } else {
-          lb.hi = lds64(wr + slot * 8);
-          lb.lo = lds32(wr + kStageW * 2 / 3 + slot * 4);  // 1-bit plane after the 2-bit plane
+          lb.hi = lds64(wr + slot_u * 8);
+          lb.lo = lds32(wr + 2048 + slot_u * 4);  // 1-bit plane after the 2-bit plane
         }
-        const uint4 sq = lds128(st + kSOff + u * p.ng * 128 + gl * 128 + s_lane);
+        const int kt0 = kt_lo + j * kWK;
+        const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt0 << 7) >> p.group_shift);
+        sq = lds128(st + 2 * kSlotW + u * p.ngw * 128 + gl * 128 + s_lane);
+      }
+      // this lane is done with the W slot after its group's last stage in it
+      {
+        const int slot_end = (j + 1) * 2 * kWK < nk ? (j + 1) * 2 * kWK : nk;
+        if (i + 2 >= slot_end) mbar_arrive(w_empty(ws.s));
+      }
+      if (i >= SA) mbar_wait(a_empty(as.s), as.ph ^ 1u);
+      if ((threadIdx.x & 255) == 0) TC_STAGE(i, 1);
+      if (active) {
+        const uint32_t at = a_at(as.s);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t scw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
           uint32_t a[4];
-          lut_dequant4(atom_index_bytes<BITS>(lb, j), lane4, lut, scw, a);
+          lut_dequant4_r128(atom_index_bytes<BITS>(lb, j), lane8, lut, scw, a);
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) sts32(st + aoff[uu][j][pp], a[pp]);
+          for (int pp = 0; pp < 4; ++pp) sts32(at + aoff[j][pp], a[pp]);
         }
       }
       fence_proxy_async_smem();  // generic-proxy A stores -> visible to the tensor core
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_ready(s));
-      mbar_arrive(empty(s));
-      if (++s == S) {
-        s = 0;
-        ph ^= 1;
-      }
+      mbar_arrive(a_full(as.s));
+      if ((threadIdx.x & 255) == 0) TC_STAGE(i, 2);
     }
-    // ===================== epilogue (warps 0..3) =====================
-    if (warp < 4) {
-      mbar_wait(acc_full, 0);
-      tc_fence_after();
-      const int n = pair * 128 + warp * 32 + lane;  // this thread's TMEM lane = output column
-      const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(trow + c0, v);
-        if (n < p.n) {
+    // ===================== epilogue (all 16 dequant warps) =====================
+    // The accumulator (TMEM lane = output column n, column = row m) goes
+    // through shared memory (the A / X rings are idle once every MMA has
+    // completed) in chunks of 32 rows: warp w reads TMEM subpartition w % 4
+    // (32 columns n) at rows [8 (w / 4), +8) of the chunk, then all 512
+    // threads write the chunk's rows to global memory with 16-byte stores.
+    mbar_wait(acc_full, 0);
+    if (threadIdx.x == 0) TC_TRACE(1, tc_now());
+    tmem_fence_after();
+    {
+      constexpr int kRows = 32;  // rows of m per chunk
+      const bool f32 = p.splits > 1;
+      const int esz = f32 ? 4 : 2;
+      const uint32_t stage_buf = base + p.a_off;  // [kRows][128] elements
+      const int sub = warp & 3;
+      const int q8 = (warp >> 2) * 8;  // this warp's 8 rows of the chunk
+      const int nl = sub * 32 + lane;  // column within the 128-column tile
+      const int n0 = pair * 128;
+      const int ncols = p.n - n0 < 128 ? p.n - n0 : 128;
+      for (int c0 = 0; c0 < BN && m0 + c0 < p.m; c0 += kRows) {
+        uint32_t v[8];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+            : "r"(tmem + (static_cast<uint32_t>(sub * 32) << 16) + static_cast<uint32_t>(c0 + q8))
+            : "memory");
+        tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int m = m0 + c0 + q;
-            if (m < p.m) {
-              const float f = __uint_as_float(v[q]);
-              if (p.splits > 1)
-                p.part[(static_cast<size_t>(z) * p.m + m) * p.n + n] = f;
-              else
-                p.y[static_cast<size_t>(m) * p.n + n] = __float2half_rn(f);
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t row = q8 + q;
+          if (f32) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(stage_buf + (row * 128 + nl) * 4), "r"(v[q]) : "memory");
+          } else {
+            const __half hv = __float2half_rn(__uint_as_float(v[q]));
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(stage_buf + (row * 128 + nl) * 2),
+                         "h"(*reinterpret_cast<const unsigned short*>(&hv))
+                         : "memory");
+          }
+        }
+        named_bar_sync(2, kDqWarps * 32);
+        // rows of 128 * esz bytes, 16-byte chunks
+        const int chunks_per_row = 128 * esz / 16;
+        const int rows = p.m - (m0 + c0) < kRows ? p.m - (m0 + c0) : kRows;
+        for (int idx = threadIdx.x; idx < rows * chunks_per_row; idx += kDqWarps * 32) {
+          const int row = idx / chunks_per_row;
+          const int ch = idx % chunks_per_row;
+          const int col = ch * 16 / esz;  // first column of the chunk
+          if (col >= ncols) continue;
+          uint4 val;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                       : "r"(stage_buf + row * 128 * esz + ch * 16));
+          const size_t m = static_cast<size_t>(m0 + c0 + row);
+          if (f32) {
+            float* dst = p.part + (static_cast<size_t>(z) * p.m + m) * p.n + n0 + col;
+            if (col + 4 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+              *reinterpret_cast<uint4*>(dst) = val;
+            } else {
+              const uint32_t e[4] = {val.x, val.y, val.z, val.w};
+              for (int q = 0; q < 4 && col + q < ncols; ++q) dst[q] = __uint_as_float(e[q]);
+            }
+          } else {
+            __half* dst = p.y + m * p.n + n0 + col;
+            if (col + 8 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+              *reinterpret_cast<uint4*>(dst) = val;
+            } else {
+              const uint32_t e[4] = {val.x, val.y, val.z, val.w};
+              const __half* h = reinterpret_cast<const __half*>(e);
+              for (int q = 0; q < 8 && col + q < ncols; ++q) dst[q] = h[q];
             }
           }
         }
+        named_bar_sync(2, kDqWarps * 32);
       }
     }
   }
-  tc_fence_before();
+  if (threadIdx.x == 0) TC_TRACE(2, tc_now());
+  tmem_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) {
-    tc_fence_after();
+    tmem_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(BN < 32 ? 32 : BN)
                  : "memory");
@@ -398,12 +488,12 @@ struct TcPlan {
   tc::Params prm{};
 };
 
-template <int BITS, int BN, int KD>
+template <int BITS, int BN>
 void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
   static thread_local int configured = -1;
   int dev = 0;
   FLUTE_TC_CUDA(cudaGetDevice(&dev));
-  auto kern = tc::qgemm_tc_kernel<BITS, BN, KD>;
+  auto kern = tc::qgemm_tc_kernel<BITS, BN>;
   if (configured != dev) {
     int optin = 0;
     FLUTE_TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -432,7 +522,34 @@ void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+#ifdef FLUTE_DIAGNOSTICS
+  // FLUTE_TC_TRACE=file: per-CTA / per-stage timeline of this launch (sync)
+  const char* trace_path = std::getenv("FLUTE_TC_TRACE");
+  tc::Params prm = pl.prm;
+  unsigned long long* tr = nullptr;
+  const size_t ctas = static_cast<size_t>(cfg.gridDim.x) * cfg.gridDim.y * cfg.gridDim.z;
+  const size_t words = ctas * 4 + ctas * 64 * 4;
+  if (trace_path) {
+    FLUTE_TC_CUDA(cudaMalloc(&tr, words * 8));
+    FLUTE_TC_CUDA(cudaMemset(tr, 0, words * 8));
+    prm.trace = tr;
+  }
+  FLUTE_TC_CUDA(cudaLaunchKernelEx(&cfg, kern, map, prm));
+  if (trace_path) {
+    FLUTE_TC_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(words);
+    FLUTE_TC_CUDA(cudaMemcpy(h.data(), tr, words * 8, cudaMemcpyDeviceToHost));
+    cudaFree(tr);
+    if (FILE* f = std::fopen(trace_path, "wb")) {
+      const unsigned long long hdr[2] = {ctas, 64};
+      std::fwrite(hdr, 8, 2, f);
+      std::fwrite(h.data(), 8, words, f);
+      std::fclose(f);
+    }
+  }
+#else
   FLUTE_TC_CUDA(cudaLaunchKernelEx(&cfg, kern, map, pl.prm));
+#endif
   if (pl.splits > 1) {
     const size_t mn = static_cast<size_t>(a.m) * a.n;
     cudaLaunchConfig_t c2{};
@@ -482,26 +599,38 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   pl.zero_part = zero_part;
   pl.bn = tc_bn(a.m, tiles_n, sms);
   if (pl.bn != 64 && pl.bn != 128 && pl.bn != 256) throw flutesim::ConfigError("FLUTE_TC_BN must be 64, 128 or 256");
-  const int kd = pl.bn == 256 ? 64 : 128;
   const long tiles = static_cast<long>((tiles_n + 1) / 2) * ((a.m + pl.bn - 1) / pl.bn);
   pl.splits = static_cast<int>(
       std::max<long>(1, std::min<long>(std::min(tiles_k, 8), sms / std::max<long>(tiles, 1))));
   if (const char* f = std::getenv("FLUTE_TC_SPLITS")) pl.splits = std::max(1, std::min(tiles_k, std::atoi(f)));
   while (pl.splits > 1 && static_cast<size_t>(pl.splits) * a.m * a.n * 4 > part_bytes) --pl.splits;
-  const int ng = std::max(1, 128 >> __builtin_ctz(static_cast<unsigned>(a.group)));
-  const size_t lut = static_cast<size_t>(1u << (2 * a.bits)) * kLutRowBytes;
+  // [vLUT | barriers | A ring (sa x 16 KB) | X ring (sx x BN*128) | W ring (sw x w_stage)]
+  const int ngw = tc::kWK * 128 / a.group + 1;  // + 1: a slot may start mid-group (g = 256)
+  const size_t lut = static_cast<size_t>(1u << (2 * a.bits)) * 128;  // compact vLUT (128-byte rows)
   const size_t bar_off = lut;
-  const size_t stage_off = (bar_off + 8 * (4 * tc::kMaxStages + 2) + 1023) / 1024 * 1024;
-  const size_t atoms = kd / 64;
-  const size_t stage_bytes = ((atoms * 16384 + atoms * static_cast<size_t>(pl.bn) * 128 +
-                               2 * static_cast<size_t>(a.bits) * 1024 * kd / 128 + 2 * ng * 128) +
-                              1023) / 1024 * 1024;
+  const size_t a_off = (bar_off + 8 * (2 * tc::kMaxW + 2 * tc::kMaxA + 2 * tc::kMaxX + 2) + 1023) / 1024 * 1024;
+  const size_t x_bytes = static_cast<size_t>(pl.bn) * 128;
+  const size_t w_stage = (2 * static_cast<size_t>(tc::kWK) * a.bits * 1024 + 2 * static_cast<size_t>(ngw) * 128 +
+                           127) / 128 * 128;
   int optin = 0, dev = 0;
   FLUTE_TC_CUDA(cudaGetDevice(&dev));
   FLUTE_TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  pl.stages = static_cast<int>(std::min<size_t>(tc::kMaxStages, (optin - stage_off) / stage_bytes));
-  if (pl.stages < 2) throw flutesim::InternalError("qgemm_tc: shared-memory plan has < 2 stages");
-  pl.smem = stage_off + pl.stages * stage_bytes;
+  // ring depths: at least A 2 / X 2 / W 3, then X up to 4 (an X tile is
+  // requested only when the MMA two+ stages back has freed its slot: the
+  // latency-critical ring, measured), A up to 4, W up to 8
+  auto used = [&](int sa_, int sx_, int sw_) {
+    return a_off + sa_ * 16384 + sx_ * x_bytes + sw_ * w_stage;
+  };
+  const size_t cap = static_cast<size_t>(optin);
+  int sa = 2, sx = 2, sw = 3;
+  if (used(sa, sx, sw) > cap) throw flutesim::InternalError("qgemm_tc: shared-memory plan does not fit");
+  while (sx < tc::kMaxX && used(sa, sx + 1, sw) <= cap) ++sx;
+  while (sa < tc::kMaxA && used(sa + 1, sx, sw) <= cap) ++sa;
+  while (sw < tc::kMaxW && used(sa, sx, sw + 1) <= cap) ++sw;
+  const size_t x_off = a_off + sa * 16384;
+  const size_t w_off = x_off + sx * x_bytes;
+  pl.stages = sw;
+  pl.smem = w_off + sw * w_stage;
   tc::Params& p = pl.prm;
   p.w = static_cast<const uint8_t*>(a.w);
   p.sc = static_cast<const uint8_t*>(a.scales);
@@ -515,18 +644,21 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   p.gp = gp;
   p.group_shift = __builtin_ctz(static_cast<unsigned>(a.group));
   p.splits = pl.splits;
-  p.stages = pl.stages;
-  p.ng = ng;
-  p.lut_bytes = static_cast<uint32_t>(lut);
+  p.sw = sw;
+  p.sx = sx;
+  p.sa = sa;
+  p.ngw = ngw;
   p.bar_off = static_cast<uint32_t>(bar_off);
-  p.stage_off = static_cast<uint32_t>(stage_off);
-  p.stage_bytes = static_cast<uint32_t>(stage_bytes);
+  p.a_off = static_cast<uint32_t>(a_off);
+  p.x_off = static_cast<uint32_t>(x_off);
+  p.w_off = static_cast<uint32_t>(w_off);
+  p.w_stage = static_cast<uint32_t>(w_stage);
   cudaStream_t st = static_cast<cudaStream_t>(a.stream);
   auto go = [&](auto bits_tag) {
     constexpr int B = decltype(bits_tag)::value;
-    if (pl.bn == 256) launch_tc<B, 256, 64>(a, pl, st);
-    else if (pl.bn == 128) launch_tc<B, 128, 128>(a, pl, st);
-    else launch_tc<B, 64, 128>(a, pl, st);
+    if (pl.bn == 256) launch_tc<B, 256>(a, pl, st);
+    else if (pl.bn == 128) launch_tc<B, 128>(a, pl, st);
+    else launch_tc<B, 64>(a, pl, st);
   };
   switch (a.bits) {
     case 2: go(std::integral_constant<int, 2>{}); break;
