@@ -252,6 +252,12 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
   if (threadIdx.x == 0) FLUTE_STAMP(8);
   // cluster mode: the receive barrier must be initialised before any peer
   // arrives on it (waited for just before the first remote access)
+  // Cluster phase 1 (every thread arrives here): barriers initialised.  Phase 2
+  // (every thread arrives when it no longer needs a peer's shared memory,
+  // every thread waits just before exit): no CTA exits while a peer may still
+  // write its receive buffer — the DSMEM lifetime rule, at the cost of rank
+  // > 0 outliving only rank 0's read of the buffer, not its whole epilogue.
+  bool cl_arrived = false;
   if (p.cluster > 1) cluster_arrive_relaxed();
   pdl_launch_dependents();
 
@@ -381,6 +387,8 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
 #pragma unroll
           for (int i = 0; i < C::kFrag; ++i) st_cluster_f32(dst + i * 128, accf[i]);
           mbar_arrive_remote(mapa_shared(recv_bar, 0));
+          asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // phase 2
+          cl_arrived = true;
           continue;
         }
         mbar_wait_cluster(recv_bar, 0);
@@ -394,6 +402,8 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
             accf[i] += v;
           }
         }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // phase 2: buffer read
+        cl_arrived = true;
         goto write_y;
       }
       if (!finished) {
@@ -468,6 +478,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
             }
       }
     }
+    if (lane == 0) FLUTE_STAMP(15);  // epilogue done (diag build)
   } else {
     // ===================== consumers =====================
     if (!FLUTE_DIAG(32)) fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
@@ -684,6 +695,15 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
   }
 
   if (threadIdx.x == 0) FLUTE_STAMP(6);
+  // cluster phase 2 (see the top): threads that have not arrived yet wait
+  // out phase 1 and arrive; then every thread waits for the whole cluster
+  if (p.cluster > 1) {
+    if (!cl_arrived) {
+      cluster_wait();
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   if (p.use_ticket) {
     __syncthreads();
     if (threadIdx.x == 0) {

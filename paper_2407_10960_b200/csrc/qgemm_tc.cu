@@ -52,6 +52,11 @@ constexpr int kXWarp = 18;  // X producer
 constexpr int kThreads = 32 * 19;
 constexpr int kUnitK = 128;
 constexpr int kMaxW = 8, kMaxA = 4, kMaxX = 4;
+// The dequantised A tiles live in tensor memory ("TS" MMA): the accumulator
+// takes columns [0, BN), A slot s columns [kAcol + 32 s, +32) (128 lanes = the
+// 128 output columns n, 32 columns = 64 k as f16 pairs).
+constexpr int kTmemCols = 512;
+constexpr int kAcol = 256;
 // A W-ring slot holds kWK whole units (128 k each) of both n-tiles: one bulk
 // copy of weights and one of scales per n-tile and slot (few, large copies).
 constexpr int kWK = 2;
@@ -70,7 +75,7 @@ struct Params {
   int splits;
   int sw, sx, sa;  // W / X / A ring depths
   int ngw;       // scale groups of one n-tile in a W slot (kWK units, + 1 for an unaligned start)
-  uint32_t bar_off, a_off, x_off, w_off, w_stage;
+  uint32_t bar_off, x_off, w_off, w_stage;
   unsigned long long* trace;  // diag build, FLUTE_TC_TRACE: [cta][4] + [cta][64 stages][4] (ns)
 };
 
@@ -114,20 +119,27 @@ constexpr uint32_t instr_desc() {
   return (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                         uint32_t idesc, uint32_t accumulate) {
+// A from tensor memory (address = column base of the K = 16 slice), B = X^T
+// from shared memory (descriptor), D in tensor memory.
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+// 16 lanes x 8 columns from the mma.sync A-fragment registers of one 16 x 16
+// atom: lane L <- (row g = L, pair t) / (row g + 8, pair t) in r0 / r1,
+// pairs t + 4 in r2 / r3 (the fragment order IS the 16x128b pattern)
+__device__ __forceinline__ void tmem_st_atom(uint32_t taddr, const uint32_t (&a)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x2.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a[0]),
+               "r"(a[1]), "r"(a[2]), "r"(a[3])
+               : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
-}
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 // Ring position of item i in a ring of `depth` slots.
@@ -155,7 +167,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kSubBytes = BITS * 1024;      // one unit's packed weights (128 k)
   constexpr int kSlotW = kWK * kSubBytes;      // one n-tile's weights in a W slot
-  constexpr uint32_t kABytes = 16384;          // [128 n][64 k] f16
   constexpr uint32_t kXBytes = BN * 128;       // [BN rows][64 k] f16
 
   const uint32_t base = smem_u32(smem);
@@ -169,7 +180,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto x_empty = [&](int s) { return bars + 8 * (2 * kMaxW + 2 * kMaxA + kMaxX + s); };
   const uint32_t acc_full = bars + 8 * (2 * kMaxW + 2 * kMaxA + 2 * kMaxX);
   const uint32_t tmem_slot = acc_full + 8;  // tcgen05.alloc writes the TMEM base here
-  auto a_at = [&](int s) { return base + p.a_off + s * kABytes; };
   auto x_at = [&](int s) { return base + p.x_off + s * kXBytes; };
   auto w_at = [&](int s) { return base + p.w_off + s * p.w_stage; };
 
@@ -202,11 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
-    // TMEM accumulator: BN fp32 columns x 128 lanes
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
-                 "n"(BN < 32 ? 32 : BN)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    // TMEM: the fp32 accumulator (BN columns) + the A ring (one CTA per SM)
+    tmem_alloc(tmem_slot, kTmemCols);
   }
   tmem_fence_before();
   __syncthreads();
@@ -262,9 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = smem_desc_sw128(a_at(as.s) + kk * 32);
           const uint64_t bd = smem_desc_sw128(x_at(xs.s) + kk * 32);
-          umma_f16(tmem, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+          umma_ts(tmem, tmem + kAcol + 32 * as.s + 8 * kk, bd, idesc, (i | kk) != 0 ? 1u : 0u);
         }
         umma_commit(a_empty(as.s));  // A / X slots free once these MMAs have read them
         umma_commit(x_empty(xs.s));
@@ -277,51 +283,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     fill_lut_r128<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
     named_bar_sync(1, kDqWarps * 32);
     const uint32_t lane8 = static_cast<uint32_t>(lane) * 8u;
-    // group grp = warp >> 3 takes stages i with i % 2 == grp; its warp wl:
-    // local k-step kl = wl & 3 of the stage's 64 k, unit u = wl >> 2
+    // group grp = warp >> 3 takes stages i with i % 2 == grp.  Its warp wl
+    // owns TMEM subpartition sp = wl & 3 (= warp % 4: the 32 output columns
+    // 32 sp .. 32 sp + 31 = unit sp >> 1, atoms 2 (sp & 1) and 2 (sp & 1) + 1)
+    // and k-steps 2 ks2, 2 ks2 + 1 of the stage (ks2 = wl >> 2).
     const int grp = warp >> 3;
     const int wl = warp & 7;
-    const int kl = wl & 3;
-    const int u = wl >> 2;
-    const int g = lane >> 2, t = lane & 3;
-    // A-tile byte offset of this lane's pair p of atom j (row n, k = kk, kk+1)
-    uint32_t aoff[4][4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int pp = 0; pp < 4; ++pp) {
-        const int n = 64 * u + 16 * j + g + 8 * (pp & 1);
-        const int kk = 16 * kl + 2 * t + 8 * (pp >> 1);
-        aoff[j][pp] = static_cast<uint32_t>((n >> 3) * 1024 + (n & 7) * 128 + (((kk >> 3) ^ (n & 7)) << 4) +
-                                            (kk & 7) * 2);
-      }
+    const int sp = wl & 3;
+    const int ks2 = wl >> 2;
+    const int u = sp >> 1;
+    const int jb = 2 * (sp & 1);  // first atom of this warp
     const uint32_t s_lane = (lane >> 2) * 16;
     const bool active = u == 0 || has_u1;
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * sp) << 16) + kAcol;
     for (int i = grp; i < nk; i += 2) {
       const int j = i / (2 * kWK);         // W slot sequence number
       const int r = (i >> 1) % kWK;        // unit within the slot
       const Slot ws(j, SW), as(i, SA);
       const int kt = kt_lo + (i >> 1), h = i & 1;
-      const int kstep = kl + 4 * h;  // k-step within the unit
-      const int slot_u = kstep * 32 + lane;
       mbar_wait(w_full(ws.s), ws.ph);
       if ((threadIdx.x & 255) == 0) TC_STAGE(i, 0);
       const uint32_t st = w_at(ws.s);
-      LaneBits<BITS> lb;
-      uint4 sq = make_uint4(0u, 0u, 0u, 0u);
+      LaneBits<BITS> lb[2];
+      uint4 sq[2];
       if (active) {
         const uint32_t wr = st + u * kSlotW + r * kSubBytes;
-        if constexpr (BITS == 4) {
-          lb.w = lds128(wr + slot_u * 16);
-        } else if constexpr (BITS == 2) {
-          lb.w = lds64(wr + slot_u * 8);
-        } else {
-          lb.hi = lds64(wr + slot_u * 8);
-          lb.lo = lds32(wr + 2048 + slot_u * 4);  // 1-bit plane after the 2-bit plane
-        }
         const int kt0 = kt_lo + j * kWK;
-        const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt0 << 7) >> p.group_shift);
-        sq = lds128(st + 2 * kSlotW + u * p.ngw * 128 + gl * 128 + s_lane);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int kstep = 2 * ks2 + q + 4 * h;  // k-step within the unit
+          const int slot_u = kstep * 32 + lane;
+          if constexpr (BITS == 4) {
+            lb[q].w = lds128(wr + slot_u * 16);
+          } else if constexpr (BITS == 2) {
+            lb[q].w = lds64(wr + slot_u * 8);
+          } else {
+            lb[q].hi = lds64(wr + slot_u * 8);
+            lb[q].lo = lds32(wr + 2048 + slot_u * 4);  // 1-bit plane after the 2-bit plane
+          }
+          const int gl = (((kt << 7) + 16 * kstep) >> p.group_shift) - ((kt0 << 7) >> p.group_shift);
+          sq[q] = lds128(st + 2 * kSlotW + u * p.ngw * 128 + gl * 128 + s_lane);
+        }
       }
       // this lane is done with the W slot after its group's last stage in it
       {
@@ -329,19 +331,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i + 2 >= slot_end) mbar_arrive(w_empty(ws.s));
       }
       if (i >= SA) mbar_wait(a_empty(as.s), as.ph ^ 1u);
+      tmem_fence_after();
       if ((threadIdx.x & 255) == 0) TC_STAGE(i, 1);
       if (active) {
-        const uint32_t at = a_at(as.s);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t scw = j == 0 ? sq.x : j == 1 ? sq.y : j == 2 ? sq.z : sq.w;
-          uint32_t a[4];
-          lut_dequant4_r128(atom_index_bytes<BITS>(lb, j), lane8, lut, scw, a);
+        for (int q = 0; q < 2; ++q) {
+          const int kl = 2 * ks2 + q;  // k-step within the 64-k stage
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) sts32(at + aoff[j][pp], a[pp]);
+          for (int jj = 0; jj < 2; ++jj) {
+            const int jt = jb + jj;
+            const uint32_t scw = jt == 0 ? sq[q].x : jt == 1 ? sq[q].y : jt == 2 ? sq[q].z : sq[q].w;
+            uint32_t a[4];
+            lut_dequant4_r128(atom_index_bytes<BITS>(lb[q], jt), lane8, lut, scw, a);
+            tmem_st_atom(t_lane + (static_cast<uint32_t>(16 * jj) << 16) + 32 * as.s + 8 * kl, a);
+          }
         }
       }
-      fence_proxy_async_smem();  // generic-proxy A stores -> visible to the tensor core
+      tmem_wait_st();
+      tmem_fence_before();
       mbar_arrive(a_full(as.s));
       if ((threadIdx.x & 255) == 0) TC_STAGE(i, 2);
     }
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int kRows = 32;  // rows of m per chunk
       const bool f32 = p.splits > 1;
       const int esz = f32 ? 4 : 2;
-      const uint32_t stage_buf = base + p.a_off;  // [kRows][128] elements
+      const uint32_t stage_buf = base + p.x_off;  // [kRows][128] elements (the idle X ring)
       const int sub = warp & 3;
       const int q8 = (warp >> 2) * 8;  // this warp's 8 rows of the chunk
       const int nl = sub * 32 + lane;  // column within the 128-column tile
@@ -426,9 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == kMmaWarp) {
     tmem_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(BN < 32 ? 32 : BN)
-                 : "memory");
+    tmem_dealloc(tmem, kTmemCols);
   }
 }
 
@@ -604,11 +609,12 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
       std::max<long>(1, std::min<long>(std::min(tiles_k, 8), sms / std::max<long>(tiles, 1))));
   if (const char* f = std::getenv("FLUTE_TC_SPLITS")) pl.splits = std::max(1, std::min(tiles_k, std::atoi(f)));
   while (pl.splits > 1 && static_cast<size_t>(pl.splits) * a.m * a.n * 4 > part_bytes) --pl.splits;
-  // [vLUT | barriers | A ring (sa x 16 KB) | X ring (sx x BN*128) | W ring (sw x w_stage)]
+  // [vLUT | barriers | X ring (sx x BN*128) | W ring (sw x w_stage)]; the A
+  // ring (sa slots of 32 columns) is in tensor memory
   const int ngw = tc::kWK * 128 / a.group + 1;  // + 1: a slot may start mid-group (g = 256)
   const size_t lut = static_cast<size_t>(1u << (2 * a.bits)) * 128;  // compact vLUT (128-byte rows)
   const size_t bar_off = lut;
-  const size_t a_off = (bar_off + 8 * (2 * tc::kMaxW + 2 * tc::kMaxA + 2 * tc::kMaxX + 2) + 1023) / 1024 * 1024;
+  const size_t x_off = (bar_off + 8 * (2 * tc::kMaxW + 2 * tc::kMaxA + 2 * tc::kMaxX + 2) + 1023) / 1024 * 1024;
   const size_t x_bytes = static_cast<size_t>(pl.bn) * 128;
   const size_t w_stage = (2 * static_cast<size_t>(tc::kWK) * a.bits * 1024 + 2 * static_cast<size_t>(ngw) * 128 +
                            127) / 128 * 128;
@@ -618,16 +624,13 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   // ring depths: at least A 2 / X 2 / W 3, then X up to 4 (an X tile is
   // requested only when the MMA two+ stages back has freed its slot: the
   // latency-critical ring, measured), A up to 4, W up to 8
-  auto used = [&](int sa_, int sx_, int sw_) {
-    return a_off + sa_ * 16384 + sx_ * x_bytes + sw_ * w_stage;
-  };
+  auto used = [&](int sx_, int sw_) { return x_off + sx_ * x_bytes + sw_ * w_stage; };
   const size_t cap = static_cast<size_t>(optin);
-  int sa = 2, sx = 2, sw = 3;
-  if (used(sa, sx, sw) > cap) throw flutesim::InternalError("qgemm_tc: shared-memory plan does not fit");
-  while (sx < tc::kMaxX && used(sa, sx + 1, sw) <= cap) ++sx;
-  while (sa < tc::kMaxA && used(sa + 1, sx, sw) <= cap) ++sa;
-  while (sw < tc::kMaxW && used(sa, sx, sw + 1) <= cap) ++sw;
-  const size_t x_off = a_off + sa * 16384;
+  const int sa = tc::kMaxA;  // (tensor memory: 4 x 32 columns above the accumulator)
+  int sx = 2, sw = 3;
+  if (used(sx, sw) > cap) throw flutesim::InternalError("qgemm_tc: shared-memory plan does not fit");
+  while (sx < tc::kMaxX && used(sx + 1, sw) <= cap) ++sx;
+  while (sw < tc::kMaxW && used(sx, sw + 1) <= cap) ++sw;
   const size_t w_off = x_off + sx * x_bytes;
   pl.stages = sw;
   pl.smem = w_off + sw * w_stage;
@@ -649,7 +652,6 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   p.sa = sa;
   p.ngw = ngw;
   p.bar_off = static_cast<uint32_t>(bar_off);
-  p.a_off = static_cast<uint32_t>(a_off);
   p.x_off = static_cast<uint32_t>(x_off);
   p.w_off = static_cast<uint32_t>(w_off);
   p.w_stage = static_cast<uint32_t>(w_stage);
