@@ -55,7 +55,7 @@ def main():
     res = F.debug_times(P, L)
     t0 = min(int(r[0][:, 0][r[0][:, 0] > 0].min()) for r in res)
     print(f"M={m} K={k} N={n} W{bits}g{group} P={P}, {L} back-to-back launches (us from first start)")
-    print("launch " + " ".join(f"{nm[:12]:>12s}" for nm in ["start", "prod_pdl_wait", "first_stage", "last_seg_end", "exit"]))
+    print("launch " + " ".join(f"{nm[:12]:>12s}" for nm in ["start", "prod_pdl_wait", "last_seg_end", "cons_exit", "epi_done(max)"]))
     for i, (stamps, _) in enumerate(res):
         t = stamps.astype(np.int64)
         def col(j, f):
@@ -63,8 +63,8 @@ def main():
             c = c[c > 0]
             return (f(c) - t0) / 1e3 if c.size else float("nan")
         print(f"{i:6d} " + " ".join(f"{v:12.2f}" for v in
-                                    [col(0, np.min), col(10, np.median), col(3, np.median),
-                                     col(5, np.max), col(6, np.max)]))
+                                    [col(0, np.min), col(10, np.median),
+                                     col(5, np.max), col(6, np.max), col(15, np.max)]))
 
 
     # CTA placement: CTAs per SM of the last launch (diag slot 13 = %smid)
