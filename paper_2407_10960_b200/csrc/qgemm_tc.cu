@@ -41,11 +41,13 @@ namespace flute_dev {
 
 namespace tc {
 
-// 16 dequant warps in two groups of 8 taking 64-k stages alternately (the
-// per-stage dequant is latency-bound: two stages in flight per SM), then
-// the producers and the MMA issuer.
+// 16 dequant warps in four groups of 4 taking 64-k stages round-robin (the
+// per-stage dequant is a latency chain — packed/scale loads, vLUT lookups,
+// tcgen05.st, wait::st — so four stages are in flight per SM), then the
+// producers and the MMA issuer.
 constexpr int kDqWarps = 16;
-constexpr int kGroupWarps = 8;
+constexpr int kGroupWarps = 4;
+constexpr int kGroups = kDqWarps / kGroupWarps;
 constexpr int kWWarp = 16;  // weights + scales producer
 constexpr int kMmaWarp = 17;
 constexpr int kXWarp = 18;  // X producer
@@ -76,7 +78,8 @@ struct Params {
   int sw, sx, sa;  // W / X / A ring depths
   int ngw;       // scale groups of one n-tile in a W slot (kWK units, + 1 for an unaligned start)
   uint32_t bar_off, x_off, w_off, w_stage;
-  unsigned long long* trace;  // diag build, FLUTE_TC_TRACE: [cta][4] + [cta][64 stages][4] (ns)
+  unsigned long long* trace;  // diag build, FLUTE_TC_TRACE: [cta][4] + [cta][64 stages][8] (ns)
+  int diag;                   // diag build, FLUTE_TC_DIAG bits: 1 skip tcgen05.st, 2 skip the MMAs
 };
 
 __device__ __forceinline__ unsigned long long tc_now() {
@@ -93,7 +96,7 @@ __device__ __forceinline__ unsigned long long tc_now() {
   do {                                                                                         \
     if (p.trace && (i) < 64)                                                                   \
       p.trace[static_cast<size_t>(gridDim.x * gridDim.y * gridDim.z) * 4 +                     \
-              ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 64 + (i)) * 4 + (slot)] = tc_now(); \
+              ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 64 + (i)) * 8 + (slot)] = tc_now(); \
   } while (0)
 #else
 #define TC_TRACE(slot, v) \
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nw = (kt_hi - kt_lo + kWK - 1) / kWK;  // W slots
       for (int j = 0; j < nw; ++j) {
         const Slot ws(j, SW);
-        if (j >= SW) mbar_wait(w_empty(ws.s), ws.ph ^ 1u);
+        if (j >= SW) mbar_wait_sleep(w_empty(ws.s), ws.ph ^ 1u);
         const int kt0 = kt_lo + j * kWK;
         const int nu = kt_hi - kt0 < kWK ? kt_hi - kt0 : kWK;
         const int glo = (kt0 * kUnitK) >> p.group_shift;
@@ -249,9 +252,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       prefetch_tmap(&tmap_x);
       pdl_wait();  // X belongs to the previous kernel in the stream
+      TC_TRACE(3, tc_now());
       for (int i = 0; i < nk; ++i) {
         const Slot xs(i, SX);
-        if (i >= SX) mbar_wait(x_empty(xs.s), xs.ph ^ 1u);
+        if (i >= SX) mbar_wait_sleep(x_empty(xs.s), xs.ph ^ 1u);
         const int kt = kt_lo + (i >> 1), h = i & 1;
         mbar_arrive_expect_tx(x_full(xs.s), kXBytes);
         tma_2d_g2s(x_at(xs.s), &tmap_x, kt * kUnitK + 64 * h, m0, x_full(xs.s));
@@ -263,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < nk; ++i) {
       const Slot as(i, SA), xs(i, SX);
       mbar_wait(a_full(as.s), as.ph);
+      if (lane == 0) TC_STAGE(i, 7);
       mbar_wait(x_full(xs.s), xs.ph);
       if (lane == 0) TC_STAGE(i, 3);
       tmem_fence_after();
@@ -270,6 +275,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint64_t bd = smem_desc_sw128(x_at(xs.s) + kk * 32);
+#ifdef FLUTE_DIAGNOSTICS
+          if (p.diag & 2) continue;
+#endif
           umma_ts(tmem, tmem + kAcol + 32 * as.s + 8 * kk, bd, idesc, (i | kk) != 0 ? 1u : 0u);
         }
         umma_commit(a_empty(as.s));  // A / X slots free once these MMAs have read them
@@ -283,35 +291,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     fill_lut_r128<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
     named_bar_sync(1, kDqWarps * 32);
     const uint32_t lane8 = static_cast<uint32_t>(lane) * 8u;
-    // group grp = warp >> 3 takes stages i with i % 2 == grp.  Its warp wl
-    // owns TMEM subpartition sp = wl & 3 (= warp % 4: the 32 output columns
-    // 32 sp .. 32 sp + 31 = unit sp >> 1, atoms 2 (sp & 1) and 2 (sp & 1) + 1)
-    // and k-steps 2 ks2, 2 ks2 + 1 of the stage (ks2 = wl >> 2).
-    const int grp = warp >> 3;
-    const int wl = warp & 7;
-    const int sp = wl & 3;
-    const int ks2 = wl >> 2;
+    // group grp = warp >> 2 takes stages i with i % 4 == grp.  Its warp owns
+    // TMEM subpartition sp = warp & 3 (the 32 output columns 32 sp .. 32 sp +
+    // 31 = unit sp >> 1, atoms 2 (sp & 1) and 2 (sp & 1) + 1) for all four
+    // k-steps of the stage.
+    const int grp = warp >> 2;
+    const int sp = warp & 3;
     const int u = sp >> 1;
     const int jb = 2 * (sp & 1);  // first atom of this warp
     const uint32_t s_lane = (lane >> 2) * 16;
     const bool active = u == 0 || has_u1;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(32 * sp) << 16) + kAcol;
-    for (int i = grp; i < nk; i += 2) {
+    for (int i = grp; i < nk; i += kGroups) {
       const int j = i / (2 * kWK);         // W slot sequence number
       const int r = (i >> 1) % kWK;        // unit within the slot
       const Slot ws(j, SW), as(i, SA);
       const int kt = kt_lo + (i >> 1), h = i & 1;
-      mbar_wait(w_full(ws.s), ws.ph);
-      if ((threadIdx.x & 255) == 0) TC_STAGE(i, 0);
+      mbar_wait_sleep(w_full(ws.s), ws.ph);
+      if ((threadIdx.x & 127) == 0) TC_STAGE(i, 0);
       const uint32_t st = w_at(ws.s);
-      LaneBits<BITS> lb[2];
-      uint4 sq[2];
+      LaneBits<BITS> lb[4];
+      uint4 sq[4];
       if (active) {
         const uint32_t wr = st + u * kSlotW + r * kSubBytes;
         const int kt0 = kt_lo + j * kWK;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int kstep = 2 * ks2 + q + 4 * h;  // k-step within the unit
+        for (int q = 0; q < 4; ++q) {
+          const int kstep = q + 4 * h;  // k-step within the unit
           const int slot_u = kstep * 32 + lane;
           if constexpr (BITS == 4) {
             lb[q].w = lds128(wr + slot_u * 16);
@@ -325,32 +331,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           sq[q] = lds128(st + 2 * kSlotW + u * p.ngw * 128 + gl * 128 + s_lane);
         }
       }
+      if ((threadIdx.x & 127) == 0 && (reinterpret_cast<const uint32_t*>(&lb[0])[0] | sq[0].x) != 0x7fffffffu) TC_STAGE(i, 6);
       // this lane is done with the W slot after its group's last stage in it
       {
         const int slot_end = (j + 1) * 2 * kWK < nk ? (j + 1) * 2 * kWK : nk;
-        if (i + 2 >= slot_end) mbar_arrive(w_empty(ws.s));
+        if (i + kGroups >= slot_end) mbar_arrive(w_empty(ws.s));
       }
-      if (i >= SA) mbar_wait(a_empty(as.s), as.ph ^ 1u);
+      if (i >= SA) mbar_wait_sleep(a_empty(as.s), as.ph ^ 1u);
       tmem_fence_after();
-      if ((threadIdx.x & 255) == 0) TC_STAGE(i, 1);
+      if ((threadIdx.x & 127) == 0) TC_STAGE(i, 1);
       if (active) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int kl = 2 * ks2 + q;  // k-step within the 64-k stage
+        for (int q = 0; q < 4; ++q) {
+          const int kl = q;  // k-step within the 64-k stage
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
             const int jt = jb + jj;
             const uint32_t scw = jt == 0 ? sq[q].x : jt == 1 ? sq[q].y : jt == 2 ? sq[q].z : sq[q].w;
             uint32_t a[4];
             lut_dequant4_r128(atom_index_bytes<BITS>(lb[q], jt), lane8, lut, scw, a);
+#ifdef FLUTE_DIAGNOSTICS
+            if (p.diag & 1) continue;
+#endif
             tmem_st_atom(t_lane + (static_cast<uint32_t>(16 * jj) << 16) + 32 * as.s + 8 * kl, a);
           }
         }
       }
+      if ((threadIdx.x & 127) == 0) TC_STAGE(i, 4);
       tmem_wait_st();
+      if ((threadIdx.x & 127) == 0) TC_STAGE(i, 5);
       tmem_fence_before();
       mbar_arrive(a_full(as.s));
-      if ((threadIdx.x & 255) == 0) TC_STAGE(i, 2);
+      if ((threadIdx.x & 127) == 0) TC_STAGE(i, 2);
     }
     // ===================== epilogue (all 16 dequant warps) =====================
     // The accumulator (TMEM lane = output column n, column = row m) goes
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // completed) in chunks of 32 rows: warp w reads TMEM subpartition w % 4
     // (32 columns n) at rows [8 (w / 4), +8) of the chunk, then all 512
     // threads write the chunk's rows to global memory with 16-byte stores.
-    mbar_wait(acc_full, 0);
+    mbar_wait_sleep(acc_full, 0);
     if (threadIdx.x == 0) TC_TRACE(1, tc_now());
     tmem_fence_after();
     {
@@ -531,9 +543,10 @@ void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
   // FLUTE_TC_TRACE=file: per-CTA / per-stage timeline of this launch (sync)
   const char* trace_path = std::getenv("FLUTE_TC_TRACE");
   tc::Params prm = pl.prm;
+  prm.diag = std::getenv("FLUTE_TC_DIAG") ? std::atoi(std::getenv("FLUTE_TC_DIAG")) : 0;
   unsigned long long* tr = nullptr;
   const size_t ctas = static_cast<size_t>(cfg.gridDim.x) * cfg.gridDim.y * cfg.gridDim.z;
-  const size_t words = ctas * 4 + ctas * 64 * 4;
+  const size_t words = ctas * 4 + ctas * 64 * 8;
   if (trace_path) {
     FLUTE_TC_CUDA(cudaMalloc(&tr, words * 8));
     FLUTE_TC_CUDA(cudaMemset(tr, 0, words * 8));
@@ -581,6 +594,7 @@ void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
 // M=512 34 vs 38 us, because BN = 256 would then need split-K).
 int tc_bn(int m, int tiles_n, int sms) {
   if (std::getenv("FLUTE_TC_BN")) return std::atoi(std::getenv("FLUTE_TC_BN"));
+  if (m <= 32) return 32;
   if (m < 128) return 64;
   const long tiles128 = static_cast<long>((tiles_n + 1) / 2) * ((m + 127) / 128);
   return m >= 256 && tiles128 > sms ? 256 : 128;
@@ -596,14 +610,20 @@ size_t tc_workspace_bytes(int m, int k, int n, int sms) {
   return splits > 1 ? static_cast<size_t>(splits) * m * n * 4 : 0;
 }
 
-bool tc_enabled(int m) { return m >= 64 && std::getenv("FLUTE_NO_TC") == nullptr; }
+// Rows from which the tcgen05 kernel takes over from the mma.sync kernel
+// (FLUTE_TC_MIN_M overrides, for measurements).
+bool tc_enabled(int m) {
+  static const int min_m = std::getenv("FLUTE_TC_MIN_M") ? std::atoi(std::getenv("FLUTE_TC_MIN_M")) : 64;
+  return m >= min_m && std::getenv("FLUTE_NO_TC") == nullptr;
+}
 
 void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool zero_part,
               void* part, size_t part_bytes) {
   TcPlan pl;
   pl.zero_part = zero_part;
   pl.bn = tc_bn(a.m, tiles_n, sms);
-  if (pl.bn != 64 && pl.bn != 128 && pl.bn != 256) throw flutesim::ConfigError("FLUTE_TC_BN must be 64, 128 or 256");
+  if (pl.bn != 32 && pl.bn != 64 && pl.bn != 128 && pl.bn != 256)
+    throw flutesim::ConfigError("FLUTE_TC_BN must be 32, 64, 128 or 256");
   const long tiles = static_cast<long>((tiles_n + 1) / 2) * ((a.m + pl.bn - 1) / pl.bn);
   pl.splits = static_cast<int>(
       std::max<long>(1, std::min<long>(std::min(tiles_k, 8), sms / std::max<long>(tiles, 1))));
@@ -660,7 +680,8 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
     constexpr int B = decltype(bits_tag)::value;
     if (pl.bn == 256) launch_tc<B, 256>(a, pl, st);
     else if (pl.bn == 128) launch_tc<B, 128>(a, pl, st);
-    else launch_tc<B, 64>(a, pl, st);
+    else if (pl.bn == 64) launch_tc<B, 64>(a, pl, st);
+    else launch_tc<B, 32>(a, pl, st);
   };
   switch (a.bits) {
     case 2: go(std::integral_constant<int, 2>{}); break;
