@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       TC_TRACE(3, tc_now());
       for (int i = 0; i < nk; ++i) {
         const Slot xs(i, SX);
-        if (i >= SX) mbar_wait_sleep(x_empty(xs.s), xs.ph ^ 1u);
+        // (one "slot empty" barrier per A / X slot pair: one commit per stage)
+        if (i >= SX) mbar_wait_sleep(a_empty(xs.s), xs.ph ^ 1u);
         const int kt = kt_lo + (i >> 1), h = i & 1;
         mbar_arrive_expect_tx(x_full(xs.s), kXBytes);
         tma_2d_g2s(x_at(xs.s), &tmap_x, kt * kUnitK + 64 * h, m0, x_full(xs.s));
@@ -280,8 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
           umma_ts(tmem, tmem + kAcol + 32 * as.s + 8 * kk, bd, idesc, (i | kk) != 0 ? 1u : 0u);
         }
-        umma_commit(a_empty(as.s));  // A / X slots free once these MMAs have read them
-        umma_commit(x_empty(xs.s));
+        umma_commit(a_empty(as.s));  // A and X slot s free once these MMAs have read them
         if (i == nk - 1) umma_commit(acc_full);
       }
       __syncwarp();
@@ -646,11 +646,14 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   // latency-critical ring, measured), A up to 4, W up to 8
   auto used = [&](int sx_, int sw_) { return x_off + sx_ * x_bytes + sw_ * w_stage; };
   const size_t cap = static_cast<size_t>(optin);
-  const int sa = tc::kMaxA;  // (tensor memory: 4 x 32 columns above the accumulator)
   int sx = 2, sw = 3;
   if (used(sx, sw) > cap) throw flutesim::InternalError("qgemm_tc: shared-memory plan does not fit");
   while (sx < tc::kMaxX && used(sx + 1, sw) <= cap) ++sx;
   while (sw < tc::kMaxW && used(sx, sw + 1) <= cap) ++sw;
+  // the A ring (tensor memory, <= kMaxA x 32 columns above the accumulator)
+  // pairs slot for slot with the X ring: one release barrier per pair
+  const int sa = sx;
+  static_assert(tc::kMaxX <= tc::kMaxA, "A / X rings pair up");
   const size_t w_off = x_off + sx * x_bytes;
   pl.stages = sw;
   pl.smem = w_off + sw * w_stage;
