@@ -464,7 +464,7 @@ def run_ours(args):
                          # ncu dram__bytes_read.sum + dram__bytes_write.sum of one
                          # W3 M=1 4096x14336 launch (profiles/); its algorithmic
                          # bytes are 22,974,480 (no re-reads)
-                         "traffic": 23003136 if args.workload == "headline" else None,
+                         "traffic": 23003904 if args.workload == "headline" else None,
                          "traffic_case": ("W3 g128 M=1 K=4096 N=14336, DRAM bytes per launch (ncu)"
                                           if args.workload == "headline" else None),
                          "kernel": ("qgemm_tc_kernel<4,BN> (+ splitk_reduce_kernel) = every launch "

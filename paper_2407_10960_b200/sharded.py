@@ -190,12 +190,21 @@ class NativeShardedWeights:
         _check(_lib.flute_sharded_info(h, C.byref(n0), C.byref(n1)))
         self.n0, self.n1 = n0.value, n1.value
 
+    def _check_x(self, x):
+        import torch
+        if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
+            raise InputError(f"x must be a cuda float16 [m][{self.k}] tensor")
+        return x.contiguous()
+
     def gemm(self, x, y=None, stream=None):
         import torch
         from . import _check, _lib, _stream_ptr
-        x = x.contiguous()
+        x = self._check_x(x)
         if y is None:
             y = torch.empty((x.shape[0], self.n), dtype=torch.float16, device=x.device)
+        elif (y.dtype != torch.float16 or y.device != x.device or tuple(y.shape) != (x.shape[0], self.n)
+              or not y.is_contiguous()):
+            raise InputError(f"y must be a contiguous float16 [{x.shape[0]}][{self.n}] tensor on {x.device}")
         _check(_lib.flute_sharded_gemm(self._h, x.data_ptr(), x.shape[0], y.data_ptr(),
                                        _stream_ptr(stream)))
         return y
@@ -203,9 +212,8 @@ class NativeShardedWeights:
     def gemm_fused(self, x, stream=None):
         """Full Y as a [m][n] view of the library's arena (no copy)."""
         import ctypes as C
-        import torch
         from . import _check, _lib, _stream_ptr
-        x = x.contiguous()
+        x = self._check_x(x)
         m = x.shape[0]
         out = C.c_void_p()
         _check(_lib.flute_sharded_gemm_fused(self._h, x.data_ptr(), m, C.byref(out),
