@@ -17,9 +17,15 @@
 //   4-bit: uint4, byte p of word j = pair 4j+p                      (8 bits/pair)
 //   2-bit: uint2, word h: low nibbles of bytes 0..3 = pairs 8h+0..3, high
 //          nibbles = pairs 8h+4..7                                   (4 bits/pair)
-//   3-bit: same nibble layout for the hi plane (hi_k<<2 | hi_k1), plus one u32
-//          lo word: bits 2c..2c+1 of byte b = lo pair (lo_k<<1 | lo_k1) of
-//          pair 4c+b.  Device index = (hi_nibble << 2) | lo2.
+//   3-bit: three u32 words A, B, C (uint2 hi = {A, B}, u32 lo = C).  The
+//          6-bit device index of pair 4j+p is (hi_k<<2|hi_k1)<<2 | (lo_k<<1|
+//          lo_k1) (the 2+1-bit plane split, FLUTE §3.1).  For atoms j = 0, 1,
+//          2 it sits in bits 0..5 of byte p of word A, B, C; atom 3's index is
+//          spread over bits 6..7 of byte p of A (index bits 0-1), B (2-3) and
+//          C (4-5).  Atoms 0-2 need no instruction at all, atom 3 two shifts
+//          folded into two LOP3s; bits 6..7 of every index byte are left as
+//          garbage, which the 256-entry table (64 entries replicated four
+//          times) ignores.
 #pragma once
 
 #include "ptx.cuh"
@@ -27,6 +33,17 @@
 namespace flute_dev {
 
 inline constexpr int kLutRowBytes = 256;
+
+// Rows of the shared-memory table for a bit width: 2^(2b), except W3, whose
+// 64-entry table is replicated four times (index bytes carry two don't-care
+// bits, see atom_index_bytes<3>).
+template <int BITS>
+inline constexpr int kTableRows = BITS == 3 ? 256 : 1 << (2 * BITS);
+
+// (m & a) | (~m & b), one LOP3
+__device__ __forceinline__ uint32_t bitselect(uint32_t m, uint32_t a, uint32_t b) {
+  return (m & a) | (~m & b);
+}
 
 template <int BITS>
 struct LaneBits;
@@ -57,11 +74,28 @@ __device__ __forceinline__ uint32_t atom_index_bytes<2>(const LaneBits<2>& lb, i
   const uint32_t w = (j >> 1) ? lb.w.y : lb.w.x;
   return (j & 1) ? ((w >> 4) & 0x0F0F0F0Fu) : (w & 0x0F0F0F0Fu);
 }
+// (bits 6..7 of each byte undefined: index a 256-entry table, or mask)
 template <>
 __device__ __forceinline__ uint32_t atom_index_bytes<3>(const LaneBits<3>& lb, int j) {
-  const uint32_t w = (j >> 1) ? lb.hi.y : lb.hi.x;
-  const uint32_t hi = (j & 1) ? ((w >> 2) & 0x3C3C3C3Cu) : ((w << 2) & 0x3C3C3C3Cu);
-  return hi | ((lb.lo >> (2 * j)) & 0x03030303u);
+  if (j == 0) return lb.hi.x;
+  if (j == 1) return lb.hi.y;
+  if (j == 2) return lb.lo;
+  // bits 0-1 from A >> 6, bits 2-3 from B >> 4, bits 4-5 from C >> 2
+  const uint32_t ab = bitselect(0x03030303u, lb.hi.x >> 6, lb.hi.y >> 4);
+  return bitselect(0x0F0F0F0Fu, ab, lb.lo >> 2);
+}
+
+// Inverse of atom_index_bytes<3>: the three lane words of 16 six-bit device
+// indices d[4j + p] (the packers' and the self-check's encoder).
+__host__ __device__ inline void pack_lane_w3(const uint32_t (&d)[16], uint32_t& a, uint32_t& b,
+                                             uint32_t& c) {
+  a = b = c = 0u;
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t d3 = d[12 + p];
+    a |= (d[p] | (d3 & 3u) << 6) << (8 * p);
+    b |= (d[4 + p] | ((d3 >> 2) & 3u) << 6) << (8 * p);
+    c |= (d[8 + p] | ((d3 >> 4) & 3u) << 6) << (8 * p);
+  }
 }
 
 // The four A-fragment registers of atom j: a[p] = vLUT[idx_p] * (s, s), with
@@ -98,14 +132,15 @@ __device__ __forceinline__ void lut_dequant4_r128(uint32_t idx_bytes, uint32_t l
 }
 template <int BITS, int NTHREADS>
 __device__ __forceinline__ void fill_lut_r128(uint32_t lut_base, const uint32_t* __restrict__ vlut, int tid) {
-  constexpr int kEntries = 1 << (2 * BITS);
+  constexpr int kEntries = kTableRows<BITS>;
+  constexpr int kSrcMask = (1 << (2 * BITS)) - 1;
   constexpr int kChunks = kEntries * 8;  // 8 x 16-byte chunks = the 32 lane copies
   constexpr int kPer = (kChunks + NTHREADS - 1) / NTHREADS;
   uint32_t v[kPer];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
     const int c = tid + i * NTHREADS;
-    v[i] = c < kChunks ? __ldg(vlut + (c >> 3)) : 0u;
+    v[i] = c < kChunks ? __ldg(vlut + ((c >> 3) & kSrcMask)) : 0u;
   }
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
@@ -134,10 +169,11 @@ __device__ __forceinline__ void lut_scale4(const uint32_t (&v)[4], uint32_t scal
 
 // Expand the 2^(2b) device-order vLUT words into the 32-copy shared table.
 // Called by `nthreads` threads with ids [0, nthreads).
-template <int BITS, int NTHREADS>
+template <int BITS, int NTHREADS, int ROWS = kTableRows<BITS>>
 __device__ __forceinline__ void fill_lut(uint32_t lut_base, const uint32_t* __restrict__ vlut,
                                          int tid) {
-  constexpr int kEntries = 1 << (2 * BITS);
+  constexpr int kEntries = ROWS;
+  constexpr int kSrcMask = (1 << (2 * BITS)) - 1;
   constexpr int kChunks = kEntries * 8;  // 8 x 16-byte chunks = the 32 lane copies
   constexpr int kPer = (kChunks + NTHREADS - 1) / NTHREADS;
   // All global loads first (one latency), then the shared stores.
@@ -145,7 +181,7 @@ __device__ __forceinline__ void fill_lut(uint32_t lut_base, const uint32_t* __re
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
     const int c = tid + i * NTHREADS;
-    v[i] = c < kChunks ? __ldg(vlut + (c >> 3)) : 0u;
+    v[i] = c < kChunks ? __ldg(vlut + ((c >> 3) & kSrcMask)) : 0u;
   }
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {

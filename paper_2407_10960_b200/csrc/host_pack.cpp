@@ -15,10 +15,12 @@
 //   4-bit: byte p of word j = idx_k << 4 | idx_k1 (a lane's 4 atoms are one
 //          16-byte LDS);
 //   2-bit: word j>>1, byte p, nibble j&1 = idx_k << 2 | idx_k1 (8 B per lane);
-//   3-bit: a 2-bit plane laid out like 2-bit with nibble hi_k << 2 | hi_k1
-//          (8 B per lane, the unit's first 2 KiB) and a 1-bit plane whose byte p
-//          holds lo_k << 1 | lo_k1 at bits 2j..2j+1 (4 B per lane, last 1 KiB);
-//          the device vLUT is permuted to index (hi_pair << 2) | lo_pair.
+//   3-bit: six-bit pair index D = (hi_k << 2 | hi_k1) << 2 | (lo_k << 1 | lo_k1)
+//          (2-bit plane hi, 1-bit plane lo; the device vLUT is permuted to this
+//          index) in three lane words A, B (8 B per lane, the unit's first
+//          2 KiB) and C (4 B per lane, last 1 KiB): byte p of A / B / C holds
+//          D of atom 0 / 1 / 2 in bits 0..5 and bits 0-1 / 2-3 / 4-5 of atom
+//          3's D in bits 6..7 (dequant.cuh atom_index_bytes<3>).
 // These are exactly the byte vectors dequant.cuh's atom_index_bytes expects.
 #include <algorithm>
 #include <cstring>
@@ -235,11 +237,16 @@ std::vector<std::uint8_t> pack_device(const std::vector<std::uint8_t>& indices, 
     } else if (bits == 2) {
       // word j>>1 of the lane, byte p, low nibble for even j, high for odd j
       unit[slot * 8 + (j >> 1) * 4 + p] |= static_cast<std::uint8_t>(((a << 2) | b) << (4 * (j & 1)));
-    } else {  // 3-bit: 2-bit plane (8 B / lane) then 1-bit plane (4 B / lane)
-      const std::uint32_t hi = ((a >> 1) << 2) | (b >> 1);
-      const std::uint32_t lo = ((a & 1u) << 1) | (b & 1u);
-      unit[slot * 8 + (j >> 1) * 4 + p] |= static_cast<std::uint8_t>(hi << (4 * (j & 1)));
-      unit[2048 + slot * 4 + p] |= static_cast<std::uint8_t>(lo << (2 * j));
+    } else {  // 3-bit: lane words A, B (8 B / lane) then C (4 B / lane)
+      const std::uint32_t d = ((((a >> 1) << 2) | (b >> 1)) << 2) | ((a & 1u) << 1) | (b & 1u);
+      auto word_byte = [&](int wi) -> std::uint8_t& {
+        return wi < 2 ? unit[slot * 8 + wi * 4 + p] : unit[2048 + slot * 4 + p];
+      };
+      if (j < 3) {
+        word_byte(j) |= static_cast<std::uint8_t>(d);
+      } else {
+        for (int wi = 0; wi < 3; ++wi) word_byte(wi) |= static_cast<std::uint8_t>(((d >> (2 * wi)) & 3u) << 6);
+      }
     }
   });
   return out;
@@ -264,16 +271,23 @@ std::vector<std::uint8_t> unpack_device(const std::vector<std::uint8_t>& dev, in
       const std::uint32_t v = unit[slot * 16 + j * 4 + p];
       a = v >> 4;
       b = v & 15u;
-    } else {
+    } else if (bits == 2) {
       const std::uint32_t nib = (unit[slot * 8 + (j >> 1) * 4 + p] >> (4 * (j & 1))) & 15u;
-      if (bits == 2) {
-        a = nib >> 2;
-        b = nib & 3u;
+      a = nib >> 2;
+      b = nib & 3u;
+    } else {
+      auto word_byte = [&](int wi) -> std::uint32_t {
+        return wi < 2 ? unit[slot * 8 + wi * 4 + p] : unit[2048 + slot * 4 + p];
+      };
+      std::uint32_t d = 0;
+      if (j < 3) {
+        d = word_byte(j) & 63u;
       } else {
-        const std::uint32_t lo = (unit[2048 + slot * 4 + p] >> (2 * j)) & 3u;
-        a = ((nib >> 2) << 1) | (lo >> 1);
-        b = ((nib & 3u) << 1) | (lo & 1u);
+        for (int wi = 0; wi < 3; ++wi) d |= (word_byte(wi) >> 6) << (2 * wi);
       }
+      const std::uint32_t hi = d >> 2, lo = d & 3u;  // hi = (a >> 1) << 2 | b >> 1
+      a = ((hi >> 2) << 1) | (lo >> 1);
+      b = ((hi & 3u) << 1) | (lo & 1u);
     }
     out[static_cast<std::size_t>(row) * n + col] = static_cast<std::uint8_t>(a);
     out[static_cast<std::size_t>(row + 1) * n + col] = static_cast<std::uint8_t>(b);

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <string>
 
+#include "dequant.cuh"
 #include "device_api.h"
 #include "flutesim/errors.hpp"
 
@@ -123,7 +124,7 @@ __global__ void pack_device_kernel(const uint8_t* __restrict__ idx, int k, int n
   const size_t ub = static_cast<size_t>(kUnitN) * kUnitK * bits / 8;
   uint8_t* unit = out + static_cast<size_t>(u) * ub;
   uint8_t bytes[16] = {};
-  uint32_t lo_word = 0;
+  uint32_t d3[16];  // 3-bit: six-bit device indices, encoded by pack_lane_w3
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -136,19 +137,20 @@ __global__ void pack_device_kernel(const uint8_t* __restrict__ idx, int k, int n
       } else if (bits == 2) {
         bytes[(j >> 1) * 4 + p] |= static_cast<uint8_t>(((a << 2) | b) << (4 * (j & 1)));
       } else {
-        const uint32_t hi = ((a >> 1) << 2) | (b >> 1);
-        const uint32_t lo = ((a & 1u) << 1) | (b & 1u);
-        bytes[(j >> 1) * 4 + p] |= static_cast<uint8_t>(hi << (4 * (j & 1)));
-        lo_word |= (lo << (2 * j)) << (8 * p);
+        d3[4 * j + p] = ((((a >> 1) << 2) | (b >> 1)) << 2) | ((a & 1u) << 1) | (b & 1u);
       }
     }
   if (bits == 4) {
     uint4* d = reinterpret_cast<uint4*>(unit + slot * 16);
     *d = *reinterpret_cast<const uint4*>(bytes);
-  } else {
+  } else if (bits == 2) {
     uint2* d = reinterpret_cast<uint2*>(unit + slot * 8);
     *d = *reinterpret_cast<const uint2*>(bytes);
-    if (bits == 3) *reinterpret_cast<uint32_t*>(unit + 2048 + slot * 4) = lo_word;
+  } else {
+    uint32_t wa, wb, wc;
+    pack_lane_w3(d3, wa, wb, wc);
+    *reinterpret_cast<uint2*>(unit + slot * 8) = make_uint2(wa, wb);
+    *reinterpret_cast<uint32_t*>(unit + 2048 + slot * 4) = wc;
   }
 }
 

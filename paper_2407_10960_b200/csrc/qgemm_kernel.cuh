@@ -96,7 +96,11 @@ template <int BITS, int BM, int UPS, int CW = 8>
 struct Cfg {
   static constexpr int kConsumerWarps = CW;
   static constexpr int kGroups = CW / 4;  // quartets
-  static constexpr int kEntries = 1 << (2 * BITS);
+  // shared-memory table rows: W3 replicates its 64 entries four times so index
+  // bytes need no masking (dequant.cuh), except at BM = 32, where the 48 KB it
+  // would add leave too few pipeline stages (indices are masked instead)
+  static constexpr int kEntries = BITS == 3 && BM == 32 ? 64 : kTableRows<BITS>;
+  static constexpr uint32_t kIndexMask = kEntries == 64 && BITS == 3 ? 0x3F3F3F3Fu : 0xFFFFFFFFu;
   static constexpr int kLutBytes = kEntries * kLutRowBytes;
   static constexpr int kSubBytes = BITS * 1024;  // 64 x 128 weights
   static constexpr int kWBytes = UPS * kSubBytes;
@@ -481,7 +485,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
     if (lane == 0) FLUTE_STAMP(15);  // epilogue done (diag build)
   } else {
     // ===================== consumers =====================
-    if (!FLUTE_DIAG(32)) fill_lut<BITS, kConsumerWarps * 32>(lut, p.vlut, threadIdx.x);
+    if (!FLUTE_DIAG(32)) fill_lut<BITS, kConsumerWarps * 32, C::kEntries>(lut, p.vlut, threadIdx.x);
     if (threadIdx.x == 0) FLUTE_STAMP(11);
     const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;
     // Quartets of 4 warps take stages round-robin (quartet h: stages i with
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
     if (threadIdx.x == 0) FLUTE_STAMP(2);
 
     // this lane's bytes within a unit for k-step ks: W4 16 B at slot*16; W2
-    // 8 B at slot*8; W3 8 B (2-bit plane) at slot*8 + 4 B (1-bit plane) at
+    // 8 B at slot*8; W3 8 B (lane words A, B) at slot*8 + 4 B (word C) at
     // 2048 + slot*4, slot = kstep*32 + lane
     const int slot0 = 2 * q4 * 32 + lane;
     const uint32_t w_lane = slot0 * (BITS == 4 ? 16 : 8);
@@ -618,7 +622,8 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
           // all 16 lookups of the k-step first, then scale + MMA per atom
           uint32_t v[4][4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) lut_lookup4(atom_index_bytes<BITS>(lb[r][ks], j), lane4, lut, v[j]);
+          for (int j = 0; j < 4; ++j)
+            lut_lookup4(atom_index_bytes<BITS>(lb[r][ks], j) & C::kIndexMask, lane4, lut, v[j]);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t scw = j == 0 ? sq[r].x : j == 1 ? sq[r].y : j == 2 ? sq[r].z : sq[r].w;

@@ -532,7 +532,7 @@ __global__ void dequant_all_kernel(const uint32_t* __restrict__ vlut, const uint
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NP = 1 << (2 * BITS);
   const uint32_t lut = smem_u32(smem);
-  fill_lut<BITS, 256>(lut, vlut, threadIdx.x);
+  fill_lut<BITS, 256, kTableRows<BITS>>(lut, vlut, threadIdx.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -553,23 +553,18 @@ __global__ void dequant_all_kernel(const uint32_t* __restrict__ vlut, const uint
       for (int j = 0; j < 4; ++j)
         wv[j] = d[4 * j] | (d[4 * j + 1] << 8) | (d[4 * j + 2] << 16) | (d[4 * j + 3] << 24);
       lb.w = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-    } else {
-      uint32_t hw[2] = {0u, 0u}, lo = 0u;
+    } else if constexpr (BITS == 2) {
+      uint32_t hw[2] = {0u, 0u};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-          const uint32_t e = d[4 * j + pp];
-          const uint32_t nib = BITS == 2 ? e : (e >> 2);
-          hw[j >> 1] |= nib << (8 * pp + 4 * (j & 1));
-          if (BITS == 3) lo |= (e & 3u) << (8 * pp + 2 * j);
-        }
-      if constexpr (BITS == 2) {
-        lb.w = make_uint2(hw[0], hw[1]);
-      } else {
-        lb.hi = make_uint2(hw[0], hw[1]);
-        lb.lo = lo;
-      }
+        for (int pp = 0; pp < 4; ++pp) hw[j >> 1] |= d[4 * j + pp] << (8 * pp + 4 * (j & 1));
+      lb.w = make_uint2(hw[0], hw[1]);
+    } else {
+      uint32_t wa, wb, wc;
+      pack_lane_w3(d, wa, wb, wc);
+      lb.hi = make_uint2(wa, wb);
+      lb.lo = wc;
     }
     const uint32_t s = scales[si];
     const uint32_t sw = s | (s << 16);
@@ -610,7 +605,7 @@ void dequant_all(const uint32_t* vlut_words, int bits, const uint16_t* scales, i
   DevBuf dv(np * 4), ds(n_scales * 2), dout(static_cast<size_t>(n_scales) * np * 4);
   FLUTE_CUDA(cudaMemcpy(dv.p, vlut_words, np * 4, cudaMemcpyHostToDevice));
   FLUTE_CUDA(cudaMemcpy(ds.p, scales, n_scales * 2, cudaMemcpyHostToDevice));
-  const int lut_bytes = np * kLutRowBytes;
+  const int lut_bytes = kTableRows<3> * kLutRowBytes;  // (the largest table)
   const int blocks = std::min(1024, n_scales);
   auto run = [&](auto kern) {
     FLUTE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lut_bytes));
