@@ -34,11 +34,11 @@ namespace flute_dev {
 
 inline constexpr int kLutRowBytes = 256;
 
-// Rows of the shared-memory table for a bit width: 2^(2b), except W3, whose
-// 64-entry table is replicated four times (index bytes carry two don't-care
-// bits, see atom_index_bytes<3>).
+// Rows of the shared-memory table: 256 for every bit width — the 2^(2b)
+// entries replicated 256 / 2^(2b) times, so index bytes may carry don't-care
+// high bits (atom_index_bytes<2>, <3>) and need no masking.
 template <int BITS>
-inline constexpr int kTableRows = BITS == 3 ? 256 : 1 << (2 * BITS);
+inline constexpr int kTableRows = 256;
 
 // (m & a) | (~m & b), one LOP3
 __device__ __forceinline__ uint32_t bitselect(uint32_t m, uint32_t a, uint32_t b) {
@@ -69,10 +69,11 @@ template <>
 __device__ __forceinline__ uint32_t atom_index_bytes<4>(const LaneBits<4>& lb, int j) {
   return j == 0 ? lb.w.x : j == 1 ? lb.w.y : j == 2 ? lb.w.z : lb.w.w;
 }
+// (bits 4..7 of each byte undefined: index a 256-row table, or mask)
 template <>
 __device__ __forceinline__ uint32_t atom_index_bytes<2>(const LaneBits<2>& lb, int j) {
   const uint32_t w = (j >> 1) ? lb.w.y : lb.w.x;
-  return (j & 1) ? ((w >> 4) & 0x0F0F0F0Fu) : (w & 0x0F0F0F0Fu);
+  return (j & 1) ? w >> 4 : w;
 }
 // (bits 6..7 of each byte undefined: index a 256-entry table, or mask)
 template <>

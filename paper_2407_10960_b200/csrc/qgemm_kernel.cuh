@@ -96,11 +96,11 @@ template <int BITS, int BM, int UPS, int CW = 8>
 struct Cfg {
   static constexpr int kConsumerWarps = CW;
   static constexpr int kGroups = CW / 4;  // quartets
-  // shared-memory table rows: W3 replicates its 64 entries four times so index
-  // bytes need no masking (dequant.cuh), except at BM = 32, where the 48 KB it
-  // would add leave too few pipeline stages (indices are masked instead)
-  static constexpr int kEntries = BITS == 3 && BM == 32 ? 64 : kTableRows<BITS>;
-  static constexpr uint32_t kIndexMask = kEntries == 64 && BITS == 3 ? 0x3F3F3F3Fu : 0xFFFFFFFFu;
+  // shared-memory table rows: W2/W3 replicate their 16/64 entries to 256 so
+  // index bytes need no masking (dequant.cuh), except at BM = 32, where the
+  // 48-60 KB it would add leave too few pipeline stages (indices are masked)
+  static constexpr int kEntries = BITS != 4 && BM == 32 ? 1 << (2 * BITS) : kTableRows<BITS>;
+  static constexpr uint32_t kIndexMask = kEntries == 256 ? 0xFFFFFFFFu : BITS == 3 ? 0x3F3F3F3Fu : 0x0F0F0F0Fu;
   static constexpr int kLutBytes = kEntries * kLutRowBytes;
   static constexpr int kSubBytes = BITS * 1024;  // 64 x 128 weights
   static constexpr int kWBytes = UPS * kSubBytes;

@@ -605,7 +605,7 @@ void dequant_all(const uint32_t* vlut_words, int bits, const uint16_t* scales, i
   DevBuf dv(np * 4), ds(n_scales * 2), dout(static_cast<size_t>(n_scales) * np * 4);
   FLUTE_CUDA(cudaMemcpy(dv.p, vlut_words, np * 4, cudaMemcpyHostToDevice));
   FLUTE_CUDA(cudaMemcpy(ds.p, scales, n_scales * 2, cudaMemcpyHostToDevice));
-  const int lut_bytes = kTableRows<3> * kLutRowBytes;  // (the largest table)
+  const int lut_bytes = kTableRows<4> * kLutRowBytes;
   const int blocks = std::min(1024, n_scales);
   auto run = [&](auto kern) {
     FLUTE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lut_bytes));

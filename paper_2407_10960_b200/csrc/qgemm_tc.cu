@@ -632,7 +632,7 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   // [vLUT | barriers | X ring (sx x BN*128) | W ring (sw x w_stage)]; the A
   // ring (sa slots of 32 columns) is in tensor memory
   const int ngw = tc::kWK * 128 / a.group + 1;  // + 1: a slot may start mid-group (g = 256)
-  const size_t lut = static_cast<size_t>(a.bits == 3 ? 256 : 1u << (2 * a.bits)) * 128;  // compact vLUT (128-byte rows; W3 replicated x4)
+  const size_t lut = static_cast<size_t>(kTableRows<4>) * 128;  // compact vLUT (128-byte rows, 256 of them)
   const size_t bar_off = lut;
   const size_t x_off = (bar_off + 8 * (2 * tc::kMaxW + 2 * tc::kMaxA + 2 * tc::kMaxX + 2) + 1023) / 1024 * 1024;
   const size_t x_bytes = static_cast<size_t>(pl.bn) * 128;
