@@ -654,6 +654,12 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   // pairs slot for slot with the X ring: one release barrier per pair
   const int sa = sx;
   static_assert(tc::kMaxX <= tc::kMaxA, "A / X rings pair up");
+  // stage i is dequantised by group i % 4 into A slot i % sa: with sa < 4 two
+  // groups would share a slot and one could pass a parity wait a whole phase
+  // early (measured: a hang with a decoupled 2-slot ring), so the plan must
+  // reach four slots
+  static_assert(tc::kMaxA == tc::kGroups, "one A slot per dequant group");
+  if (sa != tc::kGroups) throw flutesim::InternalError("qgemm_tc: shared-memory plan leaves fewer than 4 X/A slots");
   const size_t w_off = x_off + sx * x_bytes;
   pl.stages = sw;
   pl.smem = w_off + sw * w_stage;
