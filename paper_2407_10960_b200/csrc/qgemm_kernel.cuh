@@ -88,7 +88,10 @@ struct KParams {
   uint32_t recv_off;
   int diag;  // FLUTE_DIAG bits (diag build only; results are wrong when set):
              // 1 skip dequant/MMA, 2 skip weight loads, 4 skip X, 8 skip scales,
-             // 16 skip the Stream-K fixup, 32 skip the vLUT fill, 64 skip Y
+             // 16 skip the Stream-K fixup, 32 skip the vLUT fill, 64 skip Y,
+             // 128 skip the stage walk (no stage waits or copies), 256 no PDL
+             // wait in the epilogue, 512 no cluster barriers, 1024 no PDL
+             // wait in the producer
   unsigned long long* dbg;  // per-CTA timeline (diag build, FLUTE_DEBUG_TIMES)
 };
 
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
   // write its receive buffer — the DSMEM lifetime rule, at the cost of rank
   // > 0 outliving only rank 0's read of the buffer, not its whole epilogue.
   bool cl_arrived = false;
-  if (p.cluster > 1) cluster_arrive_relaxed();
+  if (p.cluster > 1 && !FLUTE_DIAG(512)) cluster_arrive_relaxed();
   pdl_launch_dependents();
 
   const int U = p.units;
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
     // ===================== producer =====================
     // The whole warp walks the stages (uniform control flow keeps addresses in
     // uniform registers); one elected lane issues each copy.
-    if (uend > ubeg) {
+    if (uend > ubeg && !FLUTE_DIAG(128)) {
       const bool leader = elect_one();
       if (leader) prefetch_tmap(&tmap_x);
       const uint64_t pol = policy_evict_first();
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
         }
       }
       FLUTE_STAMP(1);
-      if (!p.use_ticket) pdl_wait();  // X and the workspace belong to the previous kernel
+      if (!p.use_ticket && !FLUTE_DIAG(1024)) pdl_wait();  // X and the workspace belong to the previous kernel
       if (lane == 0) FLUTE_STAMP(10);
       Ring ring;
       int it = 0;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
     }
   } else if (warp == kEpilogueWarp) {
     // ===================== epilogue =====================
-    if (!p.use_ticket) pdl_wait();  // the workspace and Y belong to the previous kernel
+    if (!p.use_ticket && !FLUTE_DIAG(256)) pdl_wait();  // the workspace and Y belong to the previous kernel
     if (lane == 0) FLUTE_STAMP(12);
     int seg = 0;
     for (int tile = R.t_hi; uend > ubeg && tile >= R.t_lo; --tile, ++seg) {
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
       const int t0 = tile * tiles_k;
       const bool started = ubeg <= t0;
       const bool finished = uend >= t0 + tiles_k;
-      if (FLUTE_DIAG(16)) goto write_y;
+      if (FLUTE_DIAG(16) || FLUTE_DIAG(512)) goto write_y;
       if (p.cluster > 1) {
         // ---- cluster split-K: ranks > 0 push their partial into rank 0's
         // receive buffer through DSMEM; rank 0 adds them in rank order ----
@@ -568,6 +571,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
     // One stage of NS units [lo, lo + NS) in ring slot (s, ph).
     auto run_stage = [&](auto ns_tag, int lo, int s, uint32_t ph) {
       constexpr int NS = decltype(ns_tag)::value;
+      if (FLUTE_DIAG(128)) return;
 #ifdef FLUTE_DIAGNOSTICS
       if (trace && stage_no < 64) trace[stage_no * 3] = gtimer();
 #endif
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(threads_for(CW), OCC)
   if (threadIdx.x == 0) FLUTE_STAMP(6);
   // cluster phase 2 (see the top): threads that have not arrived yet wait
   // out phase 1 and arrive; then every thread waits for the whole cluster
-  if (p.cluster > 1) {
+  if (p.cluster > 1 && !FLUTE_DIAG(512)) {
     if (!cl_arrived) {
       cluster_wait();
       asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
