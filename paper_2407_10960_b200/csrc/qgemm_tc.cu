@@ -49,11 +49,19 @@ constexpr int kDqWarps = 16;
 constexpr int kGroupWarps = 4;
 constexpr int kGroups = kDqWarps / kGroupWarps;
 constexpr int kWWarp = 16;  // weights + scales producer
-constexpr int kMmaWarp = 17;
-constexpr int kXWarp = 18;  // X producer
-constexpr int kThreads = 32 * 19;
+constexpr int kXWarp = 17;  // X producer
+// MMA issuers: warp kMmaWarp + j takes stages i with i % kNumAcc<BN> == j and
+// accumulates into its own TMEM accumulator (columns [j*BN, (j+1)*BN)); the
+// epilogue adds the accumulators in j order.  One thread's tcgen05.mma issue
+// costs ~80-120 cycles whatever N is (tools/umma_chain.cu), so below N = 256
+// a single issuer cannot keep the tensor pipe busy; 2 issuers saturate it at
+// N = 128, 4 at N = 64.
+constexpr int kMmaWarp = 18;
+template <int BN>
+constexpr int kNumAcc = BN >= 256 ? 1 : BN >= 128 ? 2 : 4;  // = MMA issuer warps
+constexpr int threads_for_bn(int bn) { return 32 * (18 + (bn >= 256 ? 1 : bn >= 128 ? 2 : 4)); }
 constexpr int kUnitK = 128;
-constexpr int kMaxW = 8, kMaxA = 4, kMaxX = 4;
+constexpr int kMaxW = 8, kMaxA = 8, kMaxX = 8;
 // The dequantised A tiles live in tensor memory ("TS" MMA): the accumulator
 // takes columns [0, BN), A slot s columns [kAcol + 32 s, +32) (128 lanes = the
 // 128 output columns n, 32 columns = 64 k as f16 pairs).
@@ -165,7 +173,7 @@ struct Slot {
 //    canonical K-major SW128 UMMA layout), filled by the X warp after the
 //    PDL wait; freed by the MMA commit.
 template <int BITS, int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_for_bn(BN), 1)
     qgemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kSubBytes = BITS * 1024;      // one unit's packed weights (128 k)
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(x_full(s), 1);
       mbar_init(x_empty(s), 1);
     }
-    mbar_init(acc_full, 1);
+    mbar_init(acc_full, kNumAcc<BN>);  // one commit per MMA issuer warp
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -256,16 +264,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nk; ++i) {
         const Slot xs(i, SX);
         // (one "slot empty" barrier per A / X slot pair: one commit per stage)
-        if (i >= SX) mbar_wait_sleep(a_empty(xs.s), xs.ph ^ 1u);
+        // X slot xs.s is free once the MMAs of stage i - SX have completed:
+        // BN < 256 (several MMA issuers, stages retire out of order) — their
+        // own X-release commit; BN = 256 (one issuer, SX == SA) — the A-ring
+        // release of that stage (a second commit per stage costs the single
+        // issuer ~4 % there)
+        if (i >= SX) {
+          if constexpr (BN < 256) {
+            mbar_wait_sleep(x_empty(xs.s), xs.ph ^ 1u);
+          } else {
+            const Slot prev(i - SX, SA);
+            mbar_wait_sleep(a_empty(prev.s), prev.ph);
+          }
+        }
         const int kt = kt_lo + (i >> 1), h = i & 1;
         mbar_arrive_expect_tx(x_full(xs.s), kXBytes);
         tma_2d_g2s(x_at(xs.s), &tmap_x, kt * kUnitK + 64 * h, m0, x_full(xs.s));
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer =====================
+  } else if (warp >= kMmaWarp) {
+    // ===================== MMA issuers =====================
     constexpr uint32_t idesc = instr_desc<BN>();
-    for (int i = 0; i < nk; ++i) {
+    constexpr int NA = kNumAcc<BN>;
+    const int ja = warp - kMmaWarp;  // this issuer's accumulator
+    const uint32_t dacc = tmem + static_cast<uint32_t>(ja * BN);
+    for (int i = ja; ja < NA && i < nk; i += NA) {
       const Slot as(i, SA), xs(i, SX);
       mbar_wait(a_full(as.s), as.ph);
       if (lane == 0) TC_STAGE(i, 7);
@@ -279,13 +302,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FLUTE_DIAGNOSTICS
           if (p.diag & 2) continue;
 #endif
-          umma_ts(tmem, tmem + kAcol + 32 * as.s + 8 * kk, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+          umma_ts(dacc, tmem + kAcol + 32 * as.s + 8 * kk, bd, idesc, (i >= NA || kk) ? 1u : 0u);
         }
-        umma_commit(a_empty(as.s));  // A and X slot s free once these MMAs have read them
-        if (i == nk - 1) umma_commit(acc_full);
+        umma_commit(a_empty(as.s));  // this stage's A (and, BN = 256, X) slot free once read
+        if constexpr (BN < 256) umma_commit(x_empty(xs.s));
       }
       __syncwarp();
     }
+    // every issuer arrives once (an issuer without stages arrives at once)
+    if (elect_one()) umma_commit(acc_full);
+    __syncwarp();
   } else {
     // ===================== dequant warps (0..15) =====================
     fill_lut_r128<BITS, kDqWarps * 32>(lut, p.vlut, threadIdx.x);
@@ -383,14 +409,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nl = sub * 32 + lane;  // column within the 128-column tile
       const int n0 = pair * 128;
       const int ncols = p.n - n0 < 128 ? p.n - n0 : 128;
+      // accumulators written: one per issuer that had a stage
+      const int nacc = nk < kNumAcc<BN> ? nk : kNumAcc<BN>;
       for (int c0 = 0; c0 < BN && m0 + c0 < p.m; c0 += kRows) {
         uint32_t v[8];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-            : "r"(tmem + (static_cast<uint32_t>(sub * 32) << 16) + static_cast<uint32_t>(c0 + q8))
-            : "memory");
-        tmem_wait_ld();
+        for (int ja = 0; ja < nacc; ++ja) {
+          uint32_t w[8];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+              : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+              : "r"(tmem + (static_cast<uint32_t>(sub * 32) << 16) + static_cast<uint32_t>(ja * BN + c0 + q8))
+              : "memory");
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)  // fixed accumulator order: bitwise reproducible
+            v[q] = ja == 0 ? w[q] : __float_as_uint(__uint_as_float(v[q]) + __uint_as_float(w[q]));
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t row = q8 + q;
@@ -531,7 +565,7 @@ void launch_tc(const GemmArgs& a, const TcPlan& pl, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(pl.prm.tiles_n + 1) / 2,
                      static_cast<unsigned>((a.m + BN - 1) / BN), static_cast<unsigned>(pl.splits));
-  cfg.blockDim = dim3(tc::kThreads);
+  cfg.blockDim = dim3(tc::threads_for_bn(pl.bn));
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -641,25 +675,32 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   int optin = 0, dev = 0;
   FLUTE_TC_CUDA(cudaGetDevice(&dev));
   FLUTE_TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  // ring depths: at least A 2 / X 2 / W 3, then X up to 4 (an X tile is
-  // requested only when the MMA two+ stages back has freed its slot: the
-  // latency-critical ring, measured), A up to 4, W up to 8
+  // ring depths (shared memory): at least X 2 / W 3, then X up to 4 slots
+  // (8 while they stay within 64 KB), then W up to 8 slots
   auto used = [&](int sx_, int sw_) { return x_off + sx_ * x_bytes + sw_ * w_stage; };
   const size_t cap = static_cast<size_t>(optin);
   int sx = 2, sw = 3;
   if (used(sx, sw) > cap) throw flutesim::InternalError("qgemm_tc: shared-memory plan does not fit");
-  while (sx < tc::kMaxX && used(sx + 1, sw) <= cap) ++sx;
+  while (sx < tc::kMaxX && (sx < 4 || (sx + 1) * x_bytes <= 64 * 1024) && used(sx + 1, sw) <= cap) ++sx;
   while (sw < tc::kMaxW && used(sx, sw + 1) <= cap) ++sw;
   // the A ring (tensor memory, <= kMaxA x 32 columns above the accumulator)
   // pairs slot for slot with the X ring: one release barrier per pair
-  const int sa = sx;
-  static_assert(tc::kMaxX <= tc::kMaxA, "A / X rings pair up");
-  // stage i is dequantised by group i % 4 into A slot i % sa: with sa < 4 two
-  // groups would share a slot and one could pass a parity wait a whole phase
-  // early (measured: a hang with a decoupled 2-slot ring), so the plan must
-  // reach four slots
-  static_assert(tc::kMaxA == tc::kGroups, "one A slot per dequant group");
-  if (sa != tc::kGroups) throw flutesim::InternalError("qgemm_tc: shared-memory plan leaves fewer than 4 X/A slots");
+  // A ring in tensor memory: kMaxA x 32 columns above the accumulators.
+  // Stage i is dequantised by group i % 4 into A slot i % sa (sa = 8: each group
+  // alternates between two slots, dequantising a stage while the MMAs of
+  // its previous one still read the other); a slot's phases are always waited
+  // by the same group, in order.  The MMAs of a stage release its A slot and
+  // (BN < 256) its X slot; at BN = 256 X slot s is reused after the A release
+  // of the stage SX earlier.
+  // (BN = 256: four slots, one per group — its 128-cycle UMMAs keep the
+  // tensor pipe busy and a deeper A ring only adds TMEM traffic, measured
+  // 54 -> 61 us at 8192^2 M=512)
+  static_assert(tc::kMaxA % tc::kGroups == 0, "A slots shared evenly by the dequant groups");
+  const int sa = pl.bn >= 256 ? tc::kGroups : tc::kMaxA;
+  if (pl.bn >= 256 && sx > sa) sx = sa;  // (BN = 256: X slots tracked through the A-ring releases)
+  // the epilogue stages 32 fp32 rows x 128 columns through the idle X ring
+  if (static_cast<size_t>(sx) * x_bytes < 32 * 128 * 4)
+    throw flutesim::InternalError("qgemm_tc: X ring smaller than the epilogue staging buffer");
   const size_t w_off = x_off + sx * x_bytes;
   pl.stages = sw;
   pl.smem = w_off + sw * w_stage;

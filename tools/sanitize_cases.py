@@ -54,6 +54,8 @@ CASES = {
     "cluster": lambda: run("cluster split-K", 2, 1024, 256, 4, 128, env={"FLUTE_FORCE_CLUSTER": "4"}),
     "tcgen05": lambda: run("tcgen05 split-K", 128, 1024, 256, 4, 128, env={"FLUTE_TC_SPLITS": "2"}),
     "tcgen05_bn256": lambda: run("tcgen05 BN=256", 256, 512, 256, 3, 128, env={"FLUTE_TC_BN": "256"}),
+    # four MMA issuer warps / accumulators, 8-slot A ring, decoupled X ring
+    "tcgen05_bn32": lambda: run("tcgen05 BN=32", 96, 1024, 256, 3, 64, env={"FLUTE_TC_BN": "32"}),
     "default": lambda: run("default decomposition", 1, 4096, 512, 4, 128),
     "default_m32": lambda: run("default decomposition M=32", 32, 2048, 384, 3, 128),
 }
