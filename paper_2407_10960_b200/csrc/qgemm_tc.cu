@@ -647,7 +647,8 @@ size_t tc_workspace_bytes(int m, int k, int n, int sms) {
 // Rows from which the tcgen05 kernel takes over from the mma.sync kernel
 // (FLUTE_TC_MIN_M overrides, for measurements).
 bool tc_enabled(int m) {
-  static const int min_m = std::getenv("FLUTE_TC_MIN_M") ? std::atoi(std::getenv("FLUTE_TC_MIN_M")) : 64;
+  const char* e = std::getenv("FLUTE_TC_MIN_M");  // (read per call: tests switch it)
+  const int min_m = e ? std::atoi(e) : 64;
   return m >= min_m && std::getenv("FLUTE_NO_TC") == nullptr;
 }
 

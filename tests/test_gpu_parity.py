@@ -328,6 +328,31 @@ def test_qgemm_tcgen05_vs_oracle(F, orc, gpu, monkeypatch, m, k, n, bits, group,
     assert np.array_equal(dw.gemm(x).cpu().numpy().view(np.uint16), y16)
 
 
+# Several MMA issuer warps with their own TMEM accumulators (BN = 32 / 64:
+# four, BN = 128: two), the 8-slot A ring and the separately released X ring:
+# fewer stages than accumulators (k = 128: two 64-k stages), ragged m blocks,
+# split K, every bit width, and the M = 16 / 32 regime forced onto tcgen05.
+@pytest.mark.parametrize("m,k,n,bits,group,bn,splits", [
+    (64, 128, 128, 4, 128, 32, 1), (40, 256, 192, 3, 32, 32, 1), (96, 1024, 256, 2, 64, 32, 2),
+    (64, 1024, 320, 4, 128, 64, 0), (100, 512, 128, 3, 128, 64, 3), (128, 2048, 256, 4, 256, 128, 2),
+    (130, 384, 192, 2, 128, 128, 1), (16, 1024, 256, 3, 128, 32, 0), (32, 2048, 512, 4, 128, 32, 0),
+    (24, 640, 128, 3, 64, 64, 1)])
+def test_qgemm_tcgen05_multi_issuer_vs_oracle(F, orc, gpu, monkeypatch, m, k, n, bits, group, bn, splits):
+    monkeypatch.setenv("FLUTE_TC_BN", str(bn))
+    monkeypatch.setenv("FLUTE_TC_MIN_M", "16")
+    if splits:
+        monkeypatch.setenv("FLUTE_TC_SPLITS", str(splits))
+    rng = np.random.default_rng(9100 + m + k + n + bits + group + bn)
+    idx, scales, table, x16 = _case(F, orc, rng, m, k, n, bits, group)
+    y16, dw = _gemm(F, gpu, idx, scales, table, x16, bits, group)
+    y64 = orc.reference_f64(x16, idx, bits, group, scales, table)
+    ok, emax, ratio = _within(y16, y64)
+    assert ok, f"max err {emax:.4g} ({ratio:.2f} of bound)"
+    x = gpu.from_numpy(x16.view(np.float16)).cuda()
+    for _ in range(2):  # fixed accumulator order: bitwise reproducible
+        assert np.array_equal(dw.gemm(x).cpu().numpy().view(np.uint16), y16)
+
+
 def test_qgemm_tcgen05_matches_mma_path(F, orc, gpu, monkeypatch):
     """The tcgen05 path and the mma.sync path (forced with FLUTE_NO_TC) agree
     within the parity bound on a BASELINE configs[4]-style shape."""
