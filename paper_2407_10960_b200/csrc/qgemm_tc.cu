@@ -705,6 +705,9 @@ void qgemm_tc(const GemmArgs& a, int tiles_k, int tiles_n, int gp, int sms, bool
   const size_t w_off = x_off + sx * x_bytes;
   pl.stages = sw;
   pl.smem = w_off + sw * w_stage;
+  if (std::getenv("FLUTE_TC_PLAN"))  // measurement aid: print the ring plan
+    std::fprintf(stderr, "qgemm_tc m=%d k=%d n=%d bits=%d: BN=%d splits=%d sw=%d sx=%d sa=%d smem=%zu w_stage=%zu\n",
+                 a.m, a.k, a.n, a.bits, pl.bn, pl.splits, sw, sx, sa, pl.smem, w_stage);
   tc::Params& p = pl.prm;
   p.w = static_cast<const uint8_t*>(a.w);
   p.sc = static_cast<const uint8_t*>(a.scales);
