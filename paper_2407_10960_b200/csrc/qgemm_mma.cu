@@ -312,7 +312,14 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
   if (try_launch<BITS, BM, UPS, OCC, CW>(MIN, a, m_rows, x, y, workers, units, tiles_k, gp, cluster)) return
   switch (bm_for(m_rows)) {
     case 8:
-      if constexpr (BITS == 3) { FLUTE_TRY(8, 4, 2, 4, 3); }
+      // W3: four-unit stages, three of them if they fit, else two (the
+      // 256-row table leaves room for only two at M > 1 or with a cluster
+      // receive buffer; two four-unit stages measured 1-4 % faster than
+      // three-plus two-unit ones: 14336x4096 M=1 10.72 -> 10.30 us)
+      if constexpr (BITS == 3) {
+        FLUTE_TRY(8, 4, 2, 4, 3);
+        FLUTE_TRY(8, 4, 2, 4, 2);
+      }
       if constexpr (BITS == 2) {
         FLUTE_TRY(8, 4, 2, 4, 3);
         FLUTE_TRY(8, 2, 2, 8, 2);  // (two-unit stages: 8 warps measured 6 % faster than 4)
@@ -322,6 +329,9 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
     case 16:
       if constexpr (BITS == 3) { FLUTE_TRY(16, 4, 2, 4, 3); }
       if constexpr (BITS != 4) { FLUTE_TRY(16, 2, 2, 4, 3); }
+      // two-unit stages even when only two fit (W4 4096^2 M=16 6.50 -> 6.36 us,
+      // W3 14336x4096 M=16 13.69 -> 12.64 us)
+      FLUTE_TRY(16, 2, 2, 4, 2);
       FLUTE_TRY(16, 1, 2, 4, 2);
       break;
     default:
