@@ -320,6 +320,9 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
         FLUTE_TRY(8, 4, 2, 4, 3);
         FLUTE_TRY(8, 4, 2, 4, 2);
       }
+      // W4: four-unit stages, two of them (C1 4096^2 M=1 5.61 -> 5.51 us, 70B
+      // layer 28.3 -> 27.3 us; W2 measured neutral)
+      if constexpr (BITS == 4) { FLUTE_TRY(8, 4, 2, 4, 2); }
       if constexpr (BITS == 2) {
         FLUTE_TRY(8, 4, 2, 4, 3);
         FLUTE_TRY(8, 2, 2, 8, 2);  // (two-unit stages: 8 warps measured 6 % faster than 4)
