@@ -340,6 +340,7 @@ void launch_bits(const GemmArgs& a, int m_rows, const void* x, void* y, int work
     default:
       if constexpr (BITS != 4) {
         FLUTE_TRY(32, 2, 2, 4, 3);
+        FLUTE_TRY(32, 2, 2, 4, 2);  // (two two-unit stages beat one-unit ones by ~1 %)
         FLUTE_TRY(32, 1, 2, 4, 3);
         // (big cluster receive buffers: the one-CTA-per-SM kernel below)
       }
