@@ -369,7 +369,14 @@ int cluster_for(long long tiles_n, int tiles_k, int m, int bits) {
   for (int c = 8; c >= 1; c /= 2) {
     if (c > tiles_k) continue;
     const long long g = tiles_n * c;
-    if (g <= sms && 4 * g >= 3LL * sms) return c;
+    if (g <= sms && 4 * g >= 3LL * sms) {
+      // one whole tile per CTA with slots left over (e.g. N = 14336: 224 of
+      // 296): at M <= 8 Stream-K over every slot balances the SMs better
+      // (4096x14336 M=4 10.68 -> 10.30 us, M=1 neutral to -4 %; at M >= 16
+      // its fixups cost more than the balance gains)
+      if (c == 1 && g < sms && m <= 8) return 0;
+      return c;
+    }
   }
   return 0;
 }
