@@ -106,6 +106,35 @@ def test_device_layout_w4_register_order(F):
     assert np.count_nonzero(dev) == 1
 
 
+def test_device_layout_w3_lane_words(F):
+    """W3 lane words: the 6-bit pair index D = (hi_k<<2|hi_k1)<<2
+    | (lo_k<<1|lo_k1) of atoms 0/1/2 sits in bits 0..5 of byte p of word A / B
+    / C; atom 3's D is spread over bits 6..7 of byte p of A (bits 0-1), B
+    (2-3) and C (4-5).  A, B are the lane's 8 bytes in the unit's first 2 KiB,
+    C its 4 bytes in the last 1 KiB."""
+    k, n = 128, 64
+    def one(row, col, a, b):
+        idx = np.zeros((k, n), np.uint8)
+        idx[row, col], idx[row + 1, col] = a, b
+        return F.pack_device(idx, 3, 128)
+    # pair (k=10,11) at column 21: t=1, p>>1=1, j=1, g=5, p&1=0 -> byte p=2
+    a, b = 6, 5  # hi 3 / 2, lo 0 / 1 -> D = (3<<2|2)<<2 | (0<<1|1) = 57
+    dev = one(10, 21, a, b)
+    lane = 5 * 4 + 1
+    assert dev[lane * 8 + 4 + 2] == 57          # word B (atom 1), byte 2
+    assert np.count_nonzero(dev) == 1
+    # the same pair at column 53 (atom j=3, g=5): D split over A/B/C bits 6..7
+    dev = one(10, 53, a, b)
+    assert dev[lane * 8 + 0 + 2] == (57 & 3) << 6          # A byte 2
+    assert dev[lane * 8 + 4 + 2] == ((57 >> 2) & 3) << 6   # B byte 2
+    assert dev[2048 + lane * 4 + 2] == ((57 >> 4) & 3) << 6  # C byte 2
+    assert np.count_nonzero(dev) == 3
+    for col in (21, 53):
+        d = one(10, col, a, b)
+        back = F.unpack_device(d, k, n, 3, 128)
+        assert back[10, col] == a and back[11, col] == b
+
+
 def test_scales_device_layout(F):
     k, n, group = 256, 128, 64
     sc = np.arange(n * (k // group), dtype=np.uint16) + 1
